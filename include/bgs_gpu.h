@@ -1,0 +1,151 @@
+/* bgs_gpu.h — C ABI of the B200-native low-synchronization BCGS QR (paper 2507.21791).
+ *
+ * This is the drop-in boundary for the reference's CPU QR path.  The reference has no
+ * FFI layer; its boundary is the C++ API in the headers under
+ * /root/reference/proj/include/blockgs.  Each entry point below names the reference interface it replaces.
+ * Plain pointers and sizes only: no torch, no C++ types.  All matrices are column-major
+ * fp64 with an explicit leading dimension (dense_matrix.hpp:21-22 layout contract).
+ *
+ * Compute runs on hand-written sm_100a kernels (TMA + DMMA Gram, fused block update,
+ * on-device small factor ops, on-device TSQR); the single synchronization of each block
+ * step is one NCCL allreduce when the context spans several GPUs.  There is no CPU
+ * fallback: on a host without a usable B200 every compute entry point returns
+ * BGS_E_CUDA.
+ */
+#ifndef BGS_GPU_H
+#define BGS_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes: 1:1 with the exception taxonomy of errors.hpp:9-51
+ * (DimensionError, NotSpdError, SingularError, RankDeficientError, NonFiniteError,
+ * CollectiveError, ConfigError) plus CUDA/driver failures. */
+enum {
+  BGS_OK = 0,
+  BGS_E_DIMENSION = 1,
+  BGS_E_NOT_SPD = 2,
+  BGS_E_SINGULAR = 3,
+  BGS_E_RANK_DEFICIENT = 4,
+  BGS_E_NON_FINITE = 5,
+  BGS_E_COLLECTIVE = 6, /* NCCL failure or rank mismatch */
+  BGS_E_CONFIG = 7,
+  BGS_E_INTERNAL = 8,
+  BGS_E_CUDA = 9 /* no device / CUDA error / kernel image missing */
+};
+
+/* Variant ids: same order and meaning as blockgs::VariantId (variant.hpp:8-15). */
+enum {
+  BGS_BCGS = 0, /* classic BCGS: out of scope (returns BGS_E_CONFIG) */
+  BGS_BCGSI_PLUS = 1,
+  BGS_BCGSPIPI_PLUS = 2,
+  BGS_BCGSI_PLUS_P_1S = 3,
+  BGS_BCGSI_PLUS_P_2S = 4,
+  BGS_BCGSI_PLUS_1S = 5
+};
+
+#define BGS_LABELS_CAP 65536
+
+/* SyncStats (sync_stats.hpp:13-27): one event per collective rendezvous, labels in
+ * issue order, '\n'-joined, using the reference's label strings. */
+typedef struct {
+  long sync_count;
+  long words_reduced;
+  int n_events;
+  char labels[BGS_LABELS_CAP];
+} bgs_stats;
+
+/* Error detail.  For BGS_E_NOT_SPD, `pivot` is the 1-based Cholesky pivot
+ * (NotSpdError::pivot, errors.hpp:40-44) and `msg` carries the reference's semantic
+ * diagnostic (bcgs.cpp:69-80): "<variant>: <site> for block column <k> hit a Gram matrix
+ * that is not numerically positive definite (...); likely violated working assumption:
+ * O(u) * kappa(X)^p <= 1". */
+typedef struct {
+  int code;
+  int pivot;
+  long block; /* 1-based block column of a NotSpd abort, else 0 */
+  char site[96];
+  char msg[1024];
+} bgs_error;
+
+/* Per-call device timing (CUDA events on the factorization stream). */
+typedef struct {
+  double factor_ms; /* X resident on the device -> Q, R resident; excludes H2D/D2H */
+  double total_ms;  /* whole call as seen by the host */
+  long kernel_launches; /* our kernels launched by the factorization */
+} bgs_timing;
+
+typedef struct bgs_ctx bgs_ctx;
+
+/* ---- algorithm-selection API (variant.hpp:17-39, cost_model.hpp:37) --------------- */
+const char* bgs_variant_name(int variant);                 /* variant.cpp:18-34 */
+int bgs_parse_variant(const char* name, int* variant, bgs_error* err); /* variant.cpp:43-51 */
+long bgs_expected_syncs(int variant, long q);              /* variant.cpp:53-71 */
+double bgs_variant_flops(int variant, long n, long m, long s); /* cost_model.cpp:29-119 */
+int bgs_shard_rows(long n, int procs, int rank, long* row0, long* rows); /* dist_block.cpp:33-44 */
+
+/* ---- context: device, stream, NCCL communicator, workspaces -----------------------
+ * Replaces Communicator + run_spmd's per-rank setup (communicator.hpp:50-152).
+ * nranks == 1: single GPU, no NCCL.  nranks > 1: one process (or thread) per GPU;
+ * nccl_unique_id points to the 128-byte ncclUniqueId shared by all ranks. */
+int bgs_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
+                   bgs_ctx** out, bgs_error* err);
+void bgs_ctx_destroy(bgs_ctx* ctx);
+int bgs_nccl_unique_id(void* out128, bgs_error* err); /* ncclGetUniqueId via the ctx's NCCL */
+int bgs_device_info(int device, int* sm_count, long* hbm_bytes, char* name, long name_cap);
+
+/* ---- drop-in for run_factor (runner.hpp:28-29, runner.cpp:39-67) ------------------
+ * Host X (n x m, ldx) in; Q (n x m, ldq, gathered in rank order like gather_rows) and
+ * R (m x m upper, ldr; strict lower triangle exact zeros) out.  `procs` is the
+ * reference's process count: on a single-GPU context procs > 1 runs the row-sharded
+ * algorithm with `procs` shards emulated on the one device (rank-ordered reductions,
+ * one sync per collective), mirroring the reference's simulated backend.
+ * NotSpd returns BGS_E_NOT_SPD with the diagnostic in err (FactorOutcome.ok = false). */
+int bgs_factor(bgs_ctx* ctx, int variant, long n, long m, long s, int procs,
+               const double* x, long ldx, double* q, long ldq, double* r, long ldr,
+               bgs_stats* stats, bgs_timing* timing, bgs_error* err);
+
+/* ---- device-resident per-rank entry (run_variant on a DistBlockMatrix,
+ * bcgs.hpp:49-50).  This rank owns rows [row0, row0 + n_local) of the global n x m
+ * matrix (the ceil split of dist_block.cpp:37-43).  d_x / d_q are device pointers
+ * (n_local x m, leading dimensions ldx / ldq, both even).  R is replicated: written to
+ * host memory h_r (m x m, ldr) identically on every rank.  Collectives use the ctx's
+ * NCCL communicator (nranks > 1). */
+int bgs_factor_device(bgs_ctx* ctx, int variant, long n, long m, long s, long row0,
+                      long n_local, const double* d_x, long ldx, double* d_q, long ldq,
+                      double* h_r, long ldr, bgs_stats* stats, bgs_timing* timing,
+                      bgs_error* err);
+
+/* ---- inputs and verification on the device (matrix_gen.hpp:27, metrics.hpp:10-20) -- */
+/* Seeded i.i.d. N(0,1) entries X(i,j) for global rows [row0, row0+n_local): a
+ * counter-based Philox stream keyed by (seed, global row, column), so the global matrix
+ * is independent of how it is sharded.  Not the reference's mt19937_64 sequence. */
+int bgs_gen_gaussian_device(bgs_ctx* ctx, unsigned long long seed, long row0, long n_local,
+                            long m, double* d_x, long ldx, bgs_error* err);
+/* Host-side bitwise port of the reference generator's Gaussian mode
+ * (matrix_gen.cpp:18-56: mt19937_64 + Box-Muller, column-major fill). */
+int bgs_gen_gaussian_host(unsigned long long seed, long n, long m, double* x, long ldx);
+/* loss_of_orthogonality = ||Q^T Q - I||_2 and residual ||X - QR||_F / ||X||_F
+ * computed on the GPU for a (sharded) device-resident factorization; the Gram and the
+ * residual sum are reduced over ranks with NCCL. */
+/* Same metrics for host-resident X, Q, R (uploads them; single-GPU context). */
+int bgs_metrics(bgs_ctx* ctx, long n, long m, const double* x, long ldx, const double* q,
+                long ldq, const double* r, long ldr, double* loo, double* resid, bgs_error* err);
+int bgs_metrics_device(bgs_ctx* ctx, long n, long m, long n_local, const double* d_x,
+                       long ldx, const double* d_q, long ldq, const double* h_r, long ldr,
+                       double* loo, double* resid, bgs_error* err);
+
+/* ---- building blocks exposed for parity tests ------------------------------------ */
+/* Tall-skinny Gram A^T B (dense_kernels.hpp:15-24) through the K1 TMA/DMMA kernel:
+ * host in/out, out is ma x mb (ld = ma). */
+int bgs_gram(bgs_ctx* ctx, const double* a, long n, long ma, const double* b, long mb,
+             double* out, bgs_error* err);
+/* TSQR of a tall block (intraorth.hpp:22-27) through the K4 kernels: host in/out. */
+int bgs_tsqr(bgs_ctx* ctx, const double* x, long n, long s, double* q, double* r,
+             bgs_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGS_GPU_H */

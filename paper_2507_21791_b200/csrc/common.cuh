@@ -1,0 +1,142 @@
+// common.cuh — shared device helpers for the sm_100a BCGS kernels.
+//
+// PTX wrappers for mbarrier, TMA (cp.async.bulk.tensor), fp64 DMMA (mma.sync
+// m8n8k4.f64 -> SASS DMMA.8x8x4), error-free transformations, and the device status
+// word that carries the reference's abort semantics (NotSpdError / NonFiniteError,
+// errors.hpp:9-51) between kernels without host round trips.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define BGS_DEV __device__ __forceinline__
+
+namespace bgs {
+
+// ---------------------------------------------------------------------------------
+// Device status word.  The first failing kernel writes {code, pivot, block, site} and
+// every later kernel of the factorization early-exits (SURVEY.md §5 failure detection).
+// ---------------------------------------------------------------------------------
+enum StatusCode : int {
+  ST_OK = 0,
+  ST_NOT_SPD = 2,
+  ST_SINGULAR = 3,
+  ST_NON_FINITE = 5,
+};
+// Sites of rethrow_not_spd (bcgs.cpp:284, 325, 356, 194, 209).
+enum Site : int {
+  SITE_NONE = 0,
+  SITE_PROLOGUE_PYTH = 1,   // "prologue Pythagorean normalization"
+  SITE_FIRST_PASS = 2,      // "first-pass Pythagorean normalization"
+  SITE_SECOND_PASS = 3,     // "second-pass Pythagorean normalization"
+};
+struct DevStatus {
+  int code;
+  int pivot;
+  int block;  // 1-based block column
+  int site;
+  int kappa_power;
+  int pad[3];
+};
+
+BGS_DEV bool status_bad(const DevStatus* st) {
+  return *(volatile const int*)&st->code != 0;
+}
+
+// ---------------------------------------------------------------------------------
+// Shared-memory address / mbarrier / TMA
+// ---------------------------------------------------------------------------------
+BGS_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+BGS_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+BGS_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+BGS_DEV void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+BGS_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+BGS_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+BGS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 2-D tiled TMA load global -> shared, completion on an mbarrier (SASS: UTMALDG).
+BGS_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                         int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+BGS_DEV void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---------------------------------------------------------------------------------
+// fp64 tensor core: D(8x8) += A(8x4, row) * B(4x8, col).  Lane t holds A[t/4][t%4],
+// B[t%4][t/4], C/D[t/4][2*(t%4) + {0,1}].
+// ---------------------------------------------------------------------------------
+BGS_DEV void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// 128-bit shared load of two consecutive doubles.
+BGS_DEV double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+BGS_DEV double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+BGS_DEV void sts64(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------------
+// Error-free transformation: a + b = s + e exactly (Knuth TwoSum).
+// ---------------------------------------------------------------------------------
+BGS_DEV void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// Swizzled (CU_TENSOR_MAP_SWIZZLE_128B) byte offset of the 16-byte chunk `chunk`
+// (rows 2*chunk, 2*chunk+1) of tile column `col` inside a box of 8 columns x 16 rows.
+// Each box is one 1024-byte swizzle atom.
+BGS_DEV uint32_t swz(int col, int chunk) {
+  return static_cast<uint32_t>((col >> 3) * 1024 + (col & 7) * 128 + ((chunk ^ (col & 7)) << 4));
+}
+
+}  // namespace bgs

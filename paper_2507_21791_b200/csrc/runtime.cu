@@ -1,0 +1,1279 @@
+// runtime.cu — host runtime and C ABI (include/bgs_gpu.h).
+//
+// Per-variant drivers restate the control flow of the reference's bcgs.cpp
+// (onesync_impl :233-369, pipi_impl :169-219, iro_impl :135-167, single_block :83-90)
+// on top of the device kernels:
+//   K1 gram_*   (gram.cu)   — the tall products of fused_gram / tsqr_fused_gram
+//   K2 update_* (update.cu) — local_axpy_block + scale_right_block + copies
+//   K3 small_*  (small.cu)  — pyth_chol, delayed reprojection, R assembly, NotSpd
+//   K4 tsqr_*   (tsqr.cu)   — run_tsqr / householder_qr / tsqr tree
+// Every block step is enqueued on one CUDA stream; the host never waits inside the
+// factorization.  Collectives (one per sync event, recorded with the reference's labels
+// and word counts, sync_stats.hpp:13-27) are NCCL calls on a multi-GPU context; on a
+// single-GPU context with procs > 1 the ranks' shards live on the one device and the
+// cross-rank combine is done by the same deterministic kernels (the reference's
+// "simulated" backend, communicator.hpp:98-152).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cctype>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/bgs_gpu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace bgs;
+
+namespace {
+
+// ------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------
+struct Fail {
+  int code;
+  std::string msg;
+  int pivot = 0;
+  long block = 0;
+  std::string site;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+#define CUDA_OK(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) fail(BGS_E_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+void put_err(bgs_error* err, const Fail& f) {
+  if (!err) return;
+  err->code = f.code;
+  err->pivot = f.pivot;
+  err->block = f.block;
+  snprintf(err->site, sizeof err->site, "%s", f.site.c_str());
+  snprintf(err->msg, sizeof err->msg, "%s", f.msg.c_str());
+}
+void clear_err(bgs_error* err) {
+  if (err) memset(err, 0, sizeof *err);
+}
+
+// ------------------------------------------------------------------------------------
+// NCCL, loaded on demand (only multi-GPU contexts need it)
+// ------------------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+#define LOADSYM(name)                                                      \
+  api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name)); \
+  if (!api.name) return api;
+  LOADSYM(GetUniqueId)
+  LOADSYM(CommInitRank)
+  LOADSYM(CommDestroy)
+  LOADSYM(AllReduce)
+  LOADSYM(AllGather)
+  LOADSYM(GroupStart)
+  LOADSYM(GroupEnd)
+  LOADSYM(GetErrorString)
+#undef LOADSYM
+  api.ok = true;
+  return api;
+}
+
+#define NCCL_OK(expr)                                                                    \
+  do {                                                                                   \
+    ncclResult_t r_ = (expr);                                                            \
+    if (r_ != ncclSuccess) fail(BGS_E_COLLECTIVE, "%s failed: %s", #expr, nccl().GetErrorString(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// TMA descriptor encoding through the driver entry point (no -lcuda at link time)
+// ------------------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  if (fn) return fn;
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    fail(BGS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  fn = reinterpret_cast<PFN_encodeTiled>(p);
+  return fn;
+}
+
+// Column-major rows x cols fp64 matrix, box = 16 rows x 8 columns, 128-byte swizzle.
+CUtensorMap make_map(const double* base, long rows, long cols, long ld) {
+  CUtensorMap m;
+  memset(&m, 0, sizeof m);
+  if (rows <= 0 || cols <= 0) return m;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1))
+    fail(BGS_E_DIMENSION, "device matrices need 16-byte aligned columns (even leading dimension)");
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {16, 8};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(BGS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return m;
+}
+
+// ------------------------------------------------------------------------------------
+// grow-only device buffers
+// ------------------------------------------------------------------------------------
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CUDA_OK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  double* d() const { return static_cast<double*>(p); }
+};
+
+const char* kVariantNames[6] = {"BCGS", "BCGSI+", "BCGSPIPI+", "BCGSI+P-1S", "BCGSI+P-2S",
+                                "BCGSI+1S"};
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// context
+// ------------------------------------------------------------------------------------
+struct bgs_ctx {
+  int device = 0, rank = 0, nranks = 1, sms = 148;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  DBuf partial, G, scolA, scolB, sdiag, ydiag, save, r1, r2, rtop, R, status;
+  DBuf tsqr_ws, tsqr_bounds, tsqr_trees, roots, roots_all, cross_ws, cross_m, metrics;
+  std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
+  int launches = 0;
+  ~bgs_ctx() {
+    for (DBuf* b : {&partial, &G, &scolA, &scolB, &sdiag, &ydiag, &save, &r1, &r2, &rtop, &R,
+                    &status, &tsqr_ws, &tsqr_bounds, &tsqr_trees, &roots, &roots_all, &cross_ws,
+                    &cross_m, &metrics})
+      b->release();
+    for (auto& b : sx) b.release();
+    for (auto& b : sq) b.release();
+    if (comm && nccl().ok) nccl().CommDestroy(comm);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// One row shard resident on this device: rows [row0, row0 + rows) of the global matrix.
+struct Shard {
+  long row0 = 0, rows = 0;
+  const double* X = nullptr;
+  long ldx = 0;
+  double* Q = nullptr;
+  long ldq = 0;
+  CUtensorMap mapX, mapQ;
+  // TSQR leaf plan
+  int leaf_base = 0, n_leaves = 0, bound_base = 0;
+  long hmax = 0;
+};
+
+enum Src { SX = 0, SQ = 1 };
+
+struct GSpan {
+  int src = SQ;
+  int col0 = 0;
+  int ncols = 0;  // loaded columns
+  int lcols = 0;  // left-operand (output row) columns
+};
+
+struct GramSpec {
+  int nspans = 1;
+  GSpan sp[2];
+  int N = 0;
+  int rspan[32];
+  int rcol[32];
+};
+
+class Runner {
+ public:
+  bgs_ctx* c;
+  int variant;
+  long n, m, s, q;
+  int P;        // ranks of the factorization
+  bool use_nccl;
+  std::vector<Shard> sh;
+  bgs_stats* stats;
+  long words = 0;
+  DevStatus* status;
+  int tsqr_L = 0;  // total leaves across local shards
+
+  Runner(bgs_ctx* ctx, int v, long n_, long m_, long s_, int P_, bool nccl_, bgs_stats* st)
+      : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {}
+
+  void record(const char* label, long w) {
+    if (!stats) return;
+    stats->sync_count += 1;
+    stats->words_reduced += w;
+    size_t len = strlen(stats->labels);
+    if (len + strlen(label) + 2 < sizeof stats->labels) {
+      if (stats->n_events) strcat(stats->labels, "\n");
+      strcat(stats->labels, label);
+    }
+    stats->n_events += 1;
+  }
+
+  const double* colp(const Shard& x, int src, long col) const {
+    return src == SX ? x.X + (size_t)col * x.ldx : x.Q + (size_t)col * x.ldq;
+  }
+  double* qcol(const Shard& x, long col) const { return x.Q + (size_t)col * x.ldq; }
+
+  // ---------------- setup ----------------
+  void setup() {
+    const size_t ss = (size_t)s * s;
+    c->status.ensure(sizeof(DevStatus));
+    status = reinterpret_cast<DevStatus*>(c->status.p);
+    CUDA_OK(cudaMemsetAsync(status, 0, sizeof(DevStatus), c->stream));
+    c->R.ensure((size_t)m * m * sizeof(double));
+    CUDA_OK(cudaMemsetAsync(c->R.p, 0, (size_t)m * m * sizeof(double), c->stream));
+    const long Mmax = m + 2 * s + 16;
+    c->G.ensure((size_t)Mmax * 32 * sizeof(double) + 4096);
+    c->scolA.ensure((size_t)(m + s) * s * sizeof(double));
+    c->scolB.ensure((size_t)(m + s) * s * sizeof(double));
+    c->save.ensure((size_t)(m + s) * s * sizeof(double));
+    for (DBuf* b : {&c->sdiag, &c->ydiag, &c->r1, &c->r2, &c->rtop}) b->ensure(ss * sizeof(double) + 64);
+    for (auto& x : sh) {
+      x.mapX = make_map(x.X, x.rows, m, x.ldx);
+      x.mapQ = make_map(x.Q, x.rows, m, x.ldq);
+    }
+    // Gram partial slots: every shard's CTAs
+    const int boxes_max = (int)((m + 2 * s + 7) / 8) + 2;
+    const size_t per_cta = gram_partial_doubles_per_cta(boxes_max, std::min<long>(2 * s, 32));
+    c->partial.ensure(per_cta * sizeof(double) * (size_t)grid_total() + 64);
+    // TSQR leaf plan
+    const long lw = s <= 4 ? 1024 : (s <= 8 ? 512 : 256);
+    std::vector<long> bounds;
+    std::vector<int> trees;
+    int leaf = 0;
+    for (auto& x : sh) {
+      long L = x.rows <= 0 ? 1 : (x.rows + lw - 1) / lw;
+      if (x.rows > 0) L = std::max<long>(1, std::min<long>(L, x.rows / s));
+      x.leaf_base = leaf;
+      x.n_leaves = (int)L;
+      x.bound_base = (int)bounds.size();
+      x.hmax = 0;
+      for (long l = 0; l <= L; ++l) {
+        const long b = x.rows * l / L;
+        bounds.push_back(b);
+        if (l > 0) x.hmax = std::max(x.hmax, b - bounds[bounds.size() - 2]);
+      }
+      trees.push_back(leaf);
+      leaf += (int)L;
+    }
+    trees.push_back(leaf);
+    tsqr_L = leaf;
+    c->tsqr_ws.ensure(tsqr_ws_bytes(tsqr_L, (int)s) + 64);
+    c->tsqr_bounds.ensure(bounds.size() * sizeof(long));
+    c->tsqr_trees.ensure(trees.size() * sizeof(int));
+    CUDA_OK(cudaMemcpyAsync(c->tsqr_bounds.p, bounds.data(), bounds.size() * sizeof(long),
+                            cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(c->tsqr_trees.p, trees.data(), trees.size() * sizeof(int),
+                            cudaMemcpyHostToDevice, c->stream));
+    c->roots.ensure((size_t)sh.size() * ss * sizeof(double) + 64);
+    c->roots_all.ensure((size_t)P * ss * sizeof(double) + 64);
+    c->cross_ws.ensure(tsqr_ws_bytes(P, (int)s) + 64);
+    c->cross_m.ensure((size_t)P * ss * sizeof(double) + 64);
+  }
+
+  int grid_for(const Shard& x) const {
+    const int per = std::max(1, c->sms / (int)sh.size());
+    const long stages = (x.rows + 15) / 16;
+    return (int)std::max<long>(1, std::min<long>(per, stages));
+  }
+  int grid_total() const {
+    int g = 0;
+    for (auto& x : sh) g += grid_for(x);
+    return g;
+  }
+
+  // ---------------- K1 + reduction + (NCCL) allreduce ----------------
+  // Returns M (rows of the compact Gram written to c->G, ld = M).
+  int gram(const GramSpec& sp, const char* label, bool count_sync = true,
+           bool do_allreduce = true) {
+    GramParams p;
+    memset(&p, 0, sizeof p);
+    int nbox[2] = {0, 0}, lc[2] = {0, 0};
+    for (int i = 0; i < sp.nspans; ++i) {
+      nbox[i] = (sp.sp[i].ncols + 7) / 8;
+      lc[i] = sp.sp[i].lcols;
+    }
+    const bool span1_left = sp.nspans == 2 && lc[1] > 0;
+    if (span1_left && lc[0] != sp.sp[0].ncols) fail(BGS_E_INTERNAL, "gram: bad left layout");
+    p.nbox[0] = nbox[0];
+    p.nbox[1] = nbox[1];
+    p.nboxes = nbox[0] + nbox[1];
+    p.mt_out = span1_left ? p.nboxes : (lc[0] + 7) / 8;
+    p.N = sp.N;
+    for (int i = 0; i < 2; ++i) {
+      p.col0[i] = sp.sp[i].col0;
+      p.ncols[i] = sp.sp[i].ncols;
+      p.lcols[i] = lc[i];
+    }
+    for (int j = 0; j < 32; ++j)
+      p.rcol[j] = j < sp.N ? (sp.rspan[j] == 0 ? sp.rcol[j] : 8 * nbox[0] + sp.rcol[j]) : -1;
+    p.status = status;
+    const int M = lc[0] + (span1_left ? lc[1] : 0);
+    const size_t per_cta = gram_partial_doubles_per_cta(p.mt_out, p.N);
+    int cta_base = 0;
+    for (auto& x : sh) {
+      const int grid = grid_for(x);
+      if (x.rows > 0) {
+        p.map[0] = sp.sp[0].src == SX ? x.mapX : x.mapQ;
+        if (sp.nspans == 2) p.map[1] = sp.sp[1].src == SX ? x.mapX : x.mapQ;
+        p.n_rows = x.rows;
+        p.partial = c->partial.d() + per_cta * cta_base;
+        CUDA_OK(gram_partials_launch(p, grid, c->stream, &c->launches));
+      } else {
+        CUDA_OK(cudaMemsetAsync(c->partial.d() + per_cta * cta_base, 0,
+                                per_cta * grid * sizeof(double), c->stream));
+      }
+      cta_base += grid;
+    }
+    p.partial = c->partial.d();
+    CUDA_OK(gram_reduce_launch(p, cta_base, c->G.d(), c->stream, &c->launches));
+    if (use_nccl && do_allreduce)
+      NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
+                               c->stream));
+    if (count_sync) record(label, (long)M * p.N);
+    return M;
+  }
+
+  // ---------------- K2 ----------------
+  struct Upd {
+    int kp = 0;
+    bool has_a = false, has_b = false, cb_has_a = false;
+    int srcA = SQ; long colA = 0; long dstA = 0;  // dst always in Q
+    const double* CA = nullptr; long ldca = 0; const double* TA = nullptr;
+    int srcB = SX; long colB = 0; long dstB = 0;
+    const double* CB = nullptr; long ldcb = 0; const double* TB = nullptr;
+  };
+  void update(const Upd& u) {
+    for (auto& x : sh) {
+      if (x.rows <= 0) continue;
+      UpdateParams p;
+      memset(&p, 0, sizeof p);
+      p.n_rows = x.rows;
+      p.qp = x.Q;
+      p.ldq = x.ldq;
+      p.kp = u.kp;
+      p.s = (int)s;
+      p.has_a = u.has_a;
+      p.has_b = u.has_b;
+      p.cb_has_a = u.cb_has_a;
+      if (u.has_a) {
+        p.srcA = colp(x, u.srcA, u.colA);
+        p.ld_srcA = u.srcA == SX ? x.ldx : x.ldq;
+        p.dstA = qcol(x, u.dstA);
+        p.ld_dstA = x.ldq;
+        p.CA = u.CA; p.ldca = u.ldca; p.TA = u.TA; p.ldta = s;
+      }
+      if (u.has_b) {
+        p.srcB = colp(x, u.srcB, u.colB);
+        p.ld_srcB = u.srcB == SX ? x.ldx : x.ldq;
+        p.dstB = qcol(x, u.dstB);
+        p.ld_dstB = x.ldq;
+        p.CB = u.CB; p.ldcb = u.ldcb; p.TB = u.TB; p.ldtb = s;
+      }
+      p.status = status;
+      CUDA_OK(update_launch(p, c->sms, c->stream, &c->launches));
+    }
+  }
+
+  // ---------------- K3 ----------------
+  void small(SmallParams p) {
+    p.s = (int)s;
+    p.R = c->R.d();
+    p.ldr = (int)m;
+    p.status = status;
+    CUDA_OK(small_launch(p, c->stream, &c->launches));
+  }
+
+  // ---------------- K4: TSQR of an n x s block -> Q block, root R -> rout ----------------
+  // fusedG/fusedCount: a Gram computed before this call that rides in the same
+  // rendezvous (tsqr_fused_gram, intraorth.cpp:122-135).
+  void tsqr(int src, long scol_, long dcol, double* rout, int ldrout, const char* label,
+            long fused_words = 0, double* fusedG = nullptr) {
+    const size_t ss = (size_t)s * s;
+    double* ws = c->tsqr_ws.d();
+    const long* bounds = static_cast<const long*>(c->tsqr_bounds.p);
+    const int* trees = static_cast<const int*>(c->tsqr_trees.p);
+    for (auto& x : sh) {
+      CUDA_OK(tsqr_leaf_launch(colp(x, src, scol_), src == SX ? x.ldx : x.ldq, qcol(x, dcol),
+                               x.ldq, bounds + x.bound_base, x.n_leaves, x.hmax, (int)s,
+                               tsqr_ws_R(ws) + (size_t)x.leaf_base * ss, status, c->stream,
+                               &c->launches));
+    }
+    CUDA_OK(tsqr_up_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, c->roots.d(), status,
+                           c->stream, &c->launches));
+    const double* all_roots = c->roots.d();
+    if (use_nccl) {
+      NCCL_OK(nccl().GroupStart());
+      NCCL_OK(nccl().AllGather(c->roots.p, c->roots_all.p, ss, ncclDouble, c->comm, c->stream));
+      if (fusedG && fused_words > 0)
+        NCCL_OK(nccl().AllReduce(fusedG, fusedG, (size_t)fused_words, ncclDouble, ncclSum, c->comm,
+                                 c->stream));
+      NCCL_OK(nccl().GroupEnd());
+      all_roots = c->roots_all.d();
+    }
+    CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout, c->cross_m.d(),
+                              status, c->stream, &c->launches));
+    const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
+    CUDA_OK(tsqr_down_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, mtop, status, c->stream,
+                             &c->launches));
+    for (auto& x : sh) {
+      CUDA_OK(tsqr_apply_launch(qcol(x, dcol), x.ldq, bounds + x.bound_base, x.n_leaves, (int)s,
+                                tsqr_ws_M(ws, tsqr_L, (int)s) + (size_t)x.leaf_base * ss, status,
+                                c->stream, &c->launches));
+    }
+    record(label, (long)ss + fused_words);
+  }
+
+  // ---------------- variant drivers ----------------
+  static GramSpec spec1(int src, int col0, int ncols, int lcols) {
+    GramSpec g;
+    g.nspans = 1;
+    g.sp[0] = {src, col0, ncols, lcols};
+    return g;
+  }
+  static GramSpec spec2(int src0, int col0, int n0, int l0, int src1, int col1, int n1, int l1) {
+    GramSpec g;
+    g.nspans = 2;
+    g.sp[0] = {src0, col0, n0, l0};
+    g.sp[1] = {src1, col1, n1, l1};
+    return g;
+  }
+  void set_right(GramSpec& g, int span, int col, int cnt) {
+    for (int j = 0; j < cnt; ++j) {
+      g.rspan[g.N + j] = span;
+      g.rcol[g.N + j] = col + j;
+    }
+    g.N += cnt;
+  }
+
+  double* Rd() { return c->R.d(); }
+
+  // q = 1 (bcgs.cpp:83-90)
+  void single_block() { tsqr(SX, 0, 0, Rd(), (int)m, "reduce_factor_tree:tsqr"); }
+
+  // onesync_impl (bcgs.cpp:233-369)
+  void onesync(int mode, int kappa_power) {
+    if (q == 1) return single_block();
+    const int si = (int)s;
+    double* scol_cur = c->scolA.d();
+    double* scol_nxt = c->scolB.d();
+    double* sdiag = c->sdiag.d();
+    double* ydiag = c->ydiag.d();
+    // ---- prologue: TSQR(X_1) with the first Gram in the same rendezvous ----
+    {
+      const int lc = mode == OS_PYTH ? 2 * si : si;
+      GramSpec g = spec1(SX, 0, 2 * si, lc);
+      set_right(g, 0, si, si);
+      const int M = gram(g, "", /*count_sync=*/false, /*do_allreduce=*/false);
+      tsqr(SX, 0, 0, c->rtop.d(), si, "reduce_factor_tree:prologue", (long)M * si, c->G.d());
+      SmallParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_ONESYNC_PROLOGUE;
+      sp.os_mode = mode;
+      sp.kappa_power = kappa_power;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+      sp.rtop = c->rtop.d(); sp.ldrtop = si;
+      sp.scol_next = scol_cur; sp.ld_scol_next = si;
+      sp.sdiag = sdiag;
+      small(sp);
+      Upd u;
+      u.kp = si;
+      u.has_b = true;
+      u.srcB = SX; u.colB = si; u.dstB = si;
+      u.CB = scol_cur; u.ldcb = si;
+      u.TB = mode == OS_PYTH ? sdiag : nullptr;
+      update(u);
+      if (mode == OS_TSQR) tsqr(SQ, si, si, sdiag, si, "reduce_factor_tree:tsqr");
+    }
+    // ---- block steps ----
+    for (long k = 1; k < q; ++k) {
+      const int kp = (int)(k * s);
+      const bool has_next = k + 1 < q;
+      GramSpec g;
+      if (has_next) {
+        g = spec2(SQ, 0, kp + si, kp + si, SX, kp + si, si, mode == OS_PYTH ? si : 0);
+        set_right(g, 0, kp, si);
+        set_right(g, 1, 0, si);
+      } else {
+        g = spec1(SQ, 0, kp + si, kp + si);
+        set_right(g, 0, kp, si);
+      }
+      const int M = gram(g, has_next ? "fused_gram:wide" : "fused_gram:final");
+      SmallParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_ONESYNC_STEP;
+      sp.os_mode = mode;
+      sp.k = (int)k;
+      sp.kp = kp;
+      sp.has_next = has_next;
+      sp.kappa_power = kappa_power;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = g.N;
+      sp.scol_prev = scol_cur; sp.ld_scol_prev = kp;
+      sp.scol_next = scol_nxt; sp.ld_scol_next = kp + si;
+      sp.sdiag = sdiag;
+      sp.ydiag = ydiag;
+      small(sp);
+      Upd u;
+      u.kp = kp;
+      u.has_a = true;
+      u.srcA = SQ; u.colA = kp; u.dstA = kp;
+      u.CA = c->G.d(); u.ldca = M; u.TA = ydiag;
+      if (has_next) {
+        u.has_b = true;
+        u.cb_has_a = true;
+        u.srcB = SX; u.colB = kp + si; u.dstB = kp + si;
+        u.CB = scol_nxt; u.ldcb = kp + si;
+        u.TB = mode == OS_PYTH ? sdiag : nullptr;
+      }
+      update(u);
+      if (!has_next) break;
+      if (mode == OS_TSQR) tsqr(SQ, kp + si, kp + si, sdiag, si, "reduce_factor_tree:tsqr");
+      std::swap(scol_cur, scol_nxt);
+    }
+  }
+
+  // pipi_impl (bcgs.cpp:169-219)
+  void pipi() {
+    if (q == 1) return single_block();
+    const int si = (int)s;
+    tsqr(SX, 0, 0, Rd(), (int)m, "reduce_factor_tree:tsqr");
+    for (long k = 1; k < q; ++k) {
+      const int kp = (int)(k * s);
+      // [Q_{1:k} | X_k]: two spans; the reduction drops the tile padding between them
+      GramSpec g = spec2(SQ, 0, kp, kp, SX, kp, si, si);
+      set_right(g, 1, 0, si);
+      int M = gram(g, "fused_gram:proj");
+      SmallParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_PIPI_PROJ;
+      sp.k = (int)k; sp.kp = kp; sp.kappa_power = 2;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+      sp.save = c->save.d(); sp.ldsave = kp;
+      sp.sdiag = c->sdiag.d();
+      small(sp);
+      Upd u;
+      u.kp = kp;
+      u.has_a = true;
+      u.srcA = SX; u.colA = kp; u.dstA = kp;
+      u.CA = c->save.d(); u.ldca = kp; u.TA = c->sdiag.d();
+      update(u);
+      GramSpec g2 = spec1(SQ, 0, kp + si, kp + si);
+      set_right(g2, 0, kp, si);
+      M = gram(g2, "fused_gram:reproj");
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_PIPI_REPROJ;
+      sp.k = (int)k; sp.kp = kp; sp.kappa_power = 2;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+      sp.aux1 = c->save.d(); sp.ldaux1 = kp;
+      sp.sdiag = c->sdiag.d();
+      sp.ydiag = c->ydiag.d();
+      small(sp);
+      Upd u2;
+      u2.kp = kp;
+      u2.has_a = true;
+      u2.srcA = SQ; u2.colA = kp; u2.dstA = kp;
+      u2.CA = c->G.d(); u2.ldca = M; u2.TA = c->ydiag.d();
+      update(u2);
+    }
+  }
+
+  // iro_impl (bcgs.cpp:135-167)
+  void iro() {
+    if (q == 1) return single_block();
+    const int si = (int)s;
+    tsqr(SX, 0, 0, Rd(), (int)m, "reduce_factor_tree:tsqr");
+    for (long k = 1; k < q; ++k) {
+      const int kp = (int)(k * s);
+      GramSpec g = spec2(SQ, 0, kp, kp, SX, kp, si, 0);
+      set_right(g, 1, 0, si);
+      int M = gram(g, "fused_gram:proj1");
+      SmallParams sp;
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_IRO_SAVE;
+      sp.k = (int)k; sp.kp = kp;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+      sp.save = c->save.d(); sp.ldsave = kp;
+      small(sp);
+      Upd u;
+      u.kp = kp;
+      u.has_a = true;
+      u.srcA = SX; u.colA = kp; u.dstA = kp;
+      u.CA = c->save.d(); u.ldca = kp; u.TA = nullptr;
+      update(u);
+      tsqr(SQ, kp, kp, c->r1.d(), si, "reduce_factor_tree:tsqr");
+      GramSpec g2 = spec1(SQ, 0, kp + si, kp);
+      set_right(g2, 0, kp, si);
+      M = gram(g2, "fused_gram:proj2");
+      Upd u2;
+      u2.kp = kp;
+      u2.has_a = true;
+      u2.srcA = SQ; u2.colA = kp; u2.dstA = kp;
+      u2.CA = c->G.d(); u2.ldca = M; u2.TA = nullptr;
+      update(u2);
+      tsqr(SQ, kp, kp, c->r2.d(), si, "reduce_factor_tree:tsqr");
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_IRO_FINISH;
+      sp.k = (int)k; sp.kp = kp;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = 0; sp.gn = 0;
+      sp.aux1 = c->save.d(); sp.ldaux1 = kp;
+      sp.aux2 = c->r1.d(); sp.ldaux2 = si;
+      sp.rtop = c->r2.d(); sp.ldrtop = si;
+      small(sp);
+    }
+  }
+
+  void run() {
+    setup();
+    switch (variant) {
+      case BGS_BCGSI_PLUS: iro(); break;
+      case BGS_BCGSPIPI_PLUS: pipi(); break;
+      case BGS_BCGSI_PLUS_P_1S: onesync(OS_PYTH, 2); break;
+      case BGS_BCGSI_PLUS_P_2S: onesync(OS_TSQR, 1); break;
+      case BGS_BCGSI_PLUS_1S: onesync(OS_SKIP, 3); break;
+      default: fail(BGS_E_CONFIG, "variant %d is out of scope", variant);
+    }
+  }
+
+  // Converts the device status word into the reference's exception semantics.
+  void check_status() {
+    DevStatus h;
+    CUDA_OK(cudaMemcpy(&h, status, sizeof h, cudaMemcpyDeviceToHost));
+    if (h.code == 0) return;
+    Fail f;
+    f.code = h.code;
+    f.pivot = h.pivot;
+    f.block = h.block;
+    if (h.code == ST_NOT_SPD) {
+      const char* site = h.site == SITE_PROLOGUE_PYTH ? "prologue Pythagorean normalization"
+                         : h.site == SITE_FIRST_PASS  ? "first-pass Pythagorean normalization"
+                                                      : "second-pass Pythagorean normalization";
+      f.site = site;
+      std::string hyp;
+      if (h.kappa_power == 1) hyp = "O(u) * kappa(X) <= 1";
+      else if (h.kappa_power > 1) hyp = "O(u) * kappa(X)^" + std::to_string(h.kappa_power) + " <= 1";
+      char buf[1024];
+      snprintf(buf, sizeof buf,
+               "%s: %s for block column %d hit a Gram matrix that is not numerically positive "
+               "definite (cholesky pivot %d is not strictly positive)%s%s",
+               kVariantNames[variant], site, h.block, h.pivot,
+               hyp.empty() ? "" : "; likely violated working assumption: ", hyp.c_str());
+      f.msg = buf;
+    } else if (h.code == ST_NON_FINITE) {
+      f.msg = "reduction saw a NaN or infinity";
+    } else if (h.code == ST_SINGULAR) {
+      f.msg = "triangular factor has a zero at diagonal entry " + std::to_string(h.pivot);
+    } else {
+      f.msg = "device status " + std::to_string(h.code);
+    }
+    throw f;
+  }
+};
+
+void validate(int variant, long n, long m, long s, int procs) {
+  if (procs < 1) fail(BGS_E_DIMENSION, "run_spmd: procs must be >= 1");
+  if (s <= 0 || m % s != 0) fail(BGS_E_DIMENSION, "distribute: block width must divide the columns");
+  if (m == 0)
+    fail(BGS_E_DIMENSION, "bcgs: column count must be a positive multiple of the block width");
+  if (n < m)
+    fail(BGS_E_DIMENSION, "bcgs: economic factorization needs at least as many rows as columns");
+  if (variant < 0 || variant > 5) fail(BGS_E_CONFIG, "unknown variant id %d", variant);
+  if (variant == BGS_BCGS) fail(BGS_E_CONFIG, "BCGS (classic) is out of scope for the GPU path");
+  if (s > 16) fail(BGS_E_CONFIG, "block width s = %ld exceeds the supported maximum 16", s);
+  if (m > 4096) fail(BGS_E_CONFIG, "m = %ld exceeds the supported maximum 4096", m);
+}
+
+void select_device(bgs_ctx* c) { CUDA_OK(cudaSetDevice(c->device)); }
+
+}  // namespace
+
+static long even_ld(long rows) { return std::max<long>(2, (rows + 1) & ~1L); }
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+const char* bgs_variant_name(int v) { return (v >= 0 && v < 6) ? kVariantNames[v] : nullptr; }
+
+int bgs_parse_variant(const char* name, int* variant, bgs_error* err) {
+  clear_err(err);
+  std::string key(name ? name : "");
+  for (auto& ch : key) ch = (char)std::toupper((unsigned char)ch);
+  for (int v = 0; v < 6; ++v) {
+    if (key == kVariantNames[v]) {
+      if (variant) *variant = v;
+      return BGS_OK;
+    }
+  }
+  if (err) {
+    err->code = BGS_E_CONFIG;
+    snprintf(err->msg, sizeof err->msg,
+             "unknown variant '%s' (expected one of BCGS, BCGSI+, BCGSPIPI+, BCGSI+P-1S, "
+             "BCGSI+P-2S, BCGSI+1S)",
+             name ? name : "");
+  }
+  return BGS_E_CONFIG;
+}
+
+long bgs_expected_syncs(int v, long q) {
+  if (q < 1) return -1;
+  if (q == 1) return 1;
+  switch (v) {
+    case 0: return 2 * q - 1;
+    case 1: return 4 * q - 3;
+    case 2: return 2 * q - 1;
+    case 3: return q;
+    case 4: return 2 * q - 1;
+    case 5: return q;
+  }
+  return -1;
+}
+
+double bgs_variant_flops(int v, long n, long m, long s) {
+  if (s < 1 || m < 1 || m % s != 0 || n < m) return -1.0;
+  const long q = m / s;
+  const double dn = (double)n, ds = (double)s;
+  const double block_qr = 4.0 * dn * ds * ds, block_scale = dn * ds * ds;
+  auto gu = [dn](double a, double b) { return 2.0 * dn * a * b; };
+  if (q == 1) return block_qr;
+  double f = 0.0;
+  switch (v) {
+    case 0:
+      f = block_qr;
+      for (long k = 1; k < q; ++k) f += gu(k * ds, ds) * 2 + block_qr;
+      return f;
+    case 1:
+      f = block_qr;
+      for (long k = 1; k < q; ++k) f += 2.0 * (gu(k * ds, ds) + gu(k * ds, ds) + block_qr);
+      return f;
+    case 2:
+      f = block_qr;
+      for (long k = 1; k < q; ++k)
+        f += 2.0 * gu((k + 1) * ds, ds) + 2.0 * gu(k * ds, ds) + 2.0 * block_scale;
+      return f;
+    case 3:
+      f = block_qr + gu(2.0 * ds, ds) + gu(ds, ds) + block_scale;
+      for (long k = 1; k < q; ++k) {
+        const bool hn = k + 1 < q;
+        f += hn ? gu(k * ds + 2.0 * ds, 2.0 * ds) : gu(k * ds + ds, ds);
+        f += gu(k * ds, ds) + block_scale;
+        if (hn) f += gu((k + 1) * ds, ds) + block_scale;
+      }
+      return f;
+    case 5:
+      f = block_qr + gu(ds, ds) + gu(ds, ds);
+      for (long k = 1; k < q; ++k) {
+        const bool hn = k + 1 < q;
+        f += hn ? gu(k * ds + ds, 2.0 * ds) : gu(k * ds + ds, ds);
+        f += gu(k * ds, ds) + block_scale;
+        if (hn) f += gu((k + 1) * ds, ds);
+      }
+      return f;
+    case 4:
+      f = block_qr + gu(ds, ds) + gu(ds, ds) + block_qr;
+      for (long k = 1; k < q; ++k) {
+        const bool hn = k + 1 < q;
+        f += hn ? gu(k * ds + ds, 2.0 * ds) : gu(k * ds + ds, ds);
+        f += gu(k * ds, ds) + block_scale;
+        if (hn) f += gu((k + 1) * ds, ds) + block_qr;
+      }
+      return f;
+  }
+  return -1.0;
+}
+
+int bgs_shard_rows(long n, int procs, int rank, long* row0, long* rows) {
+  if (procs < 1 || rank < 0 || rank >= procs || n < 0) return BGS_E_DIMENSION;
+  const long per = (n + procs - 1) / procs;
+  const long r0 = std::min((long)rank * per, n);
+  const long r1 = std::min(r0 + per, n);
+  if (row0) *row0 = r0;
+  if (rows) *rows = r1 - r0;
+  return BGS_OK;
+}
+
+int bgs_device_info(int device, int* sm_count, long* hbm_bytes, char* name, long name_cap) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return BGS_E_CUDA;
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (hbm_bytes) *hbm_bytes = (long)prop.totalGlobalMem;
+  if (name && name_cap > 0) snprintf(name, (size_t)name_cap, "%s", prop.name);
+  return BGS_OK;
+}
+
+int bgs_nccl_unique_id(void* out128, bgs_error* err) {
+  clear_err(err);
+  try {
+    if (!nccl().ok) fail(BGS_E_COLLECTIVE, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    NCCL_OK(nccl().GetUniqueId(&id));
+    memcpy(out128, &id, sizeof id);
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_ctx_create(int device, int rank, int nranks, const void* uid, bgs_ctx** out,
+                   bgs_error* err) {
+  clear_err(err);
+  *out = nullptr;
+  bgs_ctx* c = new bgs_ctx();
+  try {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0)
+      fail(BGS_E_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+    if (device < 0 || device >= ndev) fail(BGS_E_CUDA, "device %d out of range", device);
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    CUDA_OK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(BGS_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200)", device,
+           prop.major, prop.minor);
+    c->sms = prop.multiProcessorCount;
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&c->e0));
+    CUDA_OK(cudaEventCreate(&c->e1));
+    if (nranks > 1) {
+      if (!uid) fail(BGS_E_COLLECTIVE, "nranks > 1 needs an ncclUniqueId");
+      if (!nccl().ok) fail(BGS_E_COLLECTIVE, "libnccl.so.2 could not be loaded");
+      ncclUniqueId id;
+      memcpy(&id, uid, sizeof id);
+      NCCL_OK(nccl().CommInitRank(&c->comm, nranks, id, rank));
+    }
+    *out = c;
+    return BGS_OK;
+  } catch (const Fail& f) {
+    delete c;
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+void bgs_ctx_destroy(bgs_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  delete c;
+}
+
+
+int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const double* x,
+               long ldx, double* q, long ldq, double* r, long ldr, bgs_stats* stats,
+               bgs_timing* timing, bgs_error* err) {
+  clear_err(err);
+  if (stats) memset(stats, 0, sizeof *stats);
+  if (timing) memset(timing, 0, sizeof *timing);
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    if (!c) fail(BGS_E_CUDA, "null context");
+    validate(variant, n, m, s, procs);
+    if (ldx < n || ldq < n || ldr < m) fail(BGS_E_DIMENSION, "leading dimension too small");
+    if (c->nranks > 1) fail(BGS_E_CONFIG, "bgs_factor runs on a single-GPU context; use bgs_factor_device per rank");
+    select_device(c);
+    Runner run(c, variant, n, m, s, procs, false, stats);
+    c->sx.resize(std::max<size_t>(c->sx.size(), (size_t)procs));
+    c->sq.resize(std::max<size_t>(c->sq.size(), (size_t)procs));
+    for (int rk = 0; rk < procs; ++rk) {
+      long r0, rows;
+      bgs_shard_rows(n, procs, rk, &r0, &rows);
+      Shard sh;
+      sh.row0 = r0;
+      sh.rows = rows;
+      sh.ldx = sh.ldq = even_ld(rows);
+      c->sx[rk].ensure((size_t)sh.ldx * m * sizeof(double) + 256);
+      c->sq[rk].ensure((size_t)sh.ldq * m * sizeof(double) + 256);
+      sh.X = c->sx[rk].d();
+      sh.Q = c->sq[rk].d();
+      if (rows > 0)
+        CUDA_OK(cudaMemcpy2DAsync(c->sx[rk].p, sh.ldx * sizeof(double), x + r0, ldx * sizeof(double),
+                                  rows * sizeof(double), m, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemsetAsync(c->sq[rk].p, 0, (size_t)sh.ldq * m * sizeof(double), c->stream));
+      run.sh.push_back(sh);
+    }
+    c->launches = 0;
+    CUDA_OK(cudaEventRecord(c->e0, c->stream));
+    run.run();
+    CUDA_OK(cudaEventRecord(c->e1, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    CUDA_OK(cudaGetLastError());
+    run.check_status();
+    for (int rk = 0; rk < procs; ++rk) {
+      const Shard& sh = run.sh[rk];
+      if (sh.rows > 0)
+        CUDA_OK(cudaMemcpy2DAsync(q + sh.row0, ldq * sizeof(double), sh.Q, sh.ldq * sizeof(double),
+                                  sh.rows * sizeof(double), m, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_OK(cudaMemcpy2DAsync(r, ldr * sizeof(double), c->R.p, m * sizeof(double),
+                              m * sizeof(double), m, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    if (timing) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->e0, c->e1);
+      timing->factor_ms = ms;
+      timing->kernel_launches = c->launches;
+      timing->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return BGS_OK;
+  } catch (const Fail& f) {
+    if (c && c->stream) cudaStreamSynchronize(c->stream);
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0, long n_local,
+                      const double* d_x, long ldx, double* d_q, long ldq, double* h_r, long ldr,
+                      bgs_stats* stats, bgs_timing* timing, bgs_error* err) {
+  clear_err(err);
+  if (stats) memset(stats, 0, sizeof *stats);
+  if (timing) memset(timing, 0, sizeof *timing);
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    if (!c) fail(BGS_E_CUDA, "null context");
+    validate(variant, n, m, s, c->nranks);
+    long e0r, erows;
+    bgs_shard_rows(n, c->nranks, c->rank, &e0r, &erows);
+    if (row0 != e0r || n_local != erows)
+      fail(BGS_E_DIMENSION, "rank %d must own rows [%ld, %ld) of the ceil split", c->rank, e0r,
+           e0r + erows);
+    if (ldx < n_local || ldq < n_local || ldr < m) fail(BGS_E_DIMENSION, "leading dimension too small");
+    select_device(c);
+    Runner run(c, variant, n, m, s, c->nranks, c->nranks > 1, stats);
+    Shard sh;
+    sh.row0 = row0;
+    sh.rows = n_local;
+    sh.X = d_x;
+    sh.ldx = ldx;
+    sh.Q = d_q;
+    sh.ldq = ldq;
+    run.sh.push_back(sh);
+    c->launches = 0;
+    CUDA_OK(cudaEventRecord(c->e0, c->stream));
+    run.run();
+    CUDA_OK(cudaEventRecord(c->e1, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    CUDA_OK(cudaGetLastError());
+    run.check_status();
+    if (h_r)
+      CUDA_OK(cudaMemcpy2D(h_r, ldr * sizeof(double), c->R.p, m * sizeof(double), m * sizeof(double),
+                           m, cudaMemcpyDeviceToHost));
+    if (timing) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->e0, c->e1);
+      timing->factor_ms = ms;
+      timing->kernel_launches = c->launches;
+      timing->total_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return BGS_OK;
+  } catch (const Fail& f) {
+    if (c && c->stream) cudaStreamSynchronize(c->stream);
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_gen_gaussian_device(bgs_ctx* c, unsigned long long seed, long row0, long n_local, long m,
+                            double* d_x, long ldx, bgs_error* err) {
+  clear_err(err);
+  try {
+    select_device(c);
+    CUDA_OK(gen_gaussian_launch(seed, row0, n_local, m, d_x, ldx, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+// matrix_gen.cpp:18-56 (GaussianStream + gaussian_matrix): std::mt19937_64 is fully
+// specified by the C++ standard, so the draw sequence matches the reference's bitwise
+// on the same libm.
+int bgs_gen_gaussian_host(unsigned long long seed, long n, long m, double* x, long ldx) {
+  if (n < 0 || m < 0 || ldx < n) return BGS_E_DIMENSION;
+  std::mt19937_64 g(seed);
+  bool have = false;
+  double spare = 0.0;
+  auto unit = [&g]() { return static_cast<double>(g() >> 11) * 0x1.0p-53; };
+  for (long j = 0; j < m; ++j)
+    for (long i = 0; i < n; ++i) {
+      double v;
+      if (have) {
+        have = false;
+        v = spare;
+      } else {
+        const double u1 = unit(), u2 = unit();
+        const double radius = std::sqrt(-2.0 * std::log(1.0 - u1));
+        const double angle = 2.0 * 3.141592653589793238462643383279502884 * u2;
+        spare = radius * std::sin(angle);
+        have = true;
+        v = radius * std::cos(angle);
+      }
+      x[i + (size_t)j * ldx] = v;
+    }
+  return BGS_OK;
+}
+
+int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d_x, long ldx,
+                       const double* d_q, long ldq, const double* h_r, long ldr, double* loo,
+                       double* resid, bgs_error* err) {
+  clear_err(err);
+  try {
+    select_device(c);
+    (void)n;
+    const int si = 8;
+    // Q^T Q in panels of 8 right columns through K1 (+ NCCL allreduce)
+    Runner run(c, BGS_BCGSI_PLUS_P_1S, std::max(n, m), m, 1, c->nranks, c->nranks > 1, nullptr);
+    Shard sh;
+    sh.rows = n_local;
+    sh.X = d_x; sh.ldx = ldx;
+    sh.Q = const_cast<double*>(d_q); sh.ldq = ldq;
+    run.sh.push_back(sh);
+    c->status.ensure(sizeof(DevStatus));
+    run.status = reinterpret_cast<DevStatus*>(c->status.p);
+    CUDA_OK(cudaMemsetAsync(run.status, 0, sizeof(DevStatus), c->stream));
+    run.sh[0].mapX = make_map(d_x, n_local, m, ldx);
+    run.sh[0].mapQ = make_map(d_q, n_local, m, ldq);
+    const size_t per_cta = gram_partial_doubles_per_cta((int)((m + 7) / 8) + 1, si);
+    c->partial.ensure(per_cta * sizeof(double) * (size_t)run.grid_total() + 64);
+    c->G.ensure((size_t)(m + 16) * 32 * sizeof(double) + 4096);
+    std::vector<double> gram((size_t)m * m), panel((size_t)m * si);
+    for (long j0 = 0; j0 < m; j0 += si) {
+      const int nb = (int)std::min<long>(si, m - j0);
+      GramSpec g = Runner::spec1(SQ, 0, (int)m, (int)m);
+      run.set_right(g, 0, (int)j0, nb);
+      run.gram(g, "", false, true);
+      CUDA_OK(cudaMemcpyAsync(panel.data(), c->G.p, (size_t)m * nb * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaStreamSynchronize(c->stream));
+      for (int jj = 0; jj < nb; ++jj)
+        for (long i = 0; i < m; ++i) gram[i + (size_t)(j0 + jj) * m] = panel[i + (size_t)jj * m];
+    }
+    for (long i = 0; i < m; ++i) gram[i + i * m] -= 1.0;
+    // two_norm (dense_kernels.cpp:205-239): power iteration on a^T a
+    std::vector<double> ata((size_t)m * m);
+    for (long j = 0; j < m; ++j)
+      for (long i = 0; i < m; ++i) {
+        double acc = 0.0;
+        for (long k = 0; k < m; ++k) acc += gram[k + i * m] * gram[k + j * m];
+        ata[i + j * m] = acc;
+      }
+    std::vector<double> v(m), w(m);
+    double nv = 0.0;
+    for (long i = 0; i < m; ++i) { v[i] = 1.0 + (double)(i % 13) / 16.0; nv += v[i] * v[i]; }
+    nv = std::sqrt(nv);
+    for (auto& t : v) t /= nv;
+    double lambda = 0.0, lambda_prev = 0.0;
+    for (int it = 0; it < 5000; ++it) {
+      double nw = 0.0;
+      for (long i = 0; i < m; ++i) {
+        double acc = 0.0;
+        for (long k = 0; k < m; ++k) acc += ata[i + k * m] * v[k];
+        w[i] = acc;
+        nw += acc * acc;
+      }
+      nw = std::sqrt(nw);
+      if (nw == 0.0) { lambda = 0.0; break; }
+      lambda = nw;
+      for (long i = 0; i < m; ++i) v[i] = w[i] / nw;
+      if (std::fabs(lambda - lambda_prev) <= 1e-10 * lambda) break;
+      lambda_prev = lambda;
+    }
+    if (loo) *loo = std::sqrt(lambda);
+    // residual
+    // per-CTA (d^2, x^2) double-double partials: <= 2*sms CTAs x 2 double2, then 2 results
+    const size_t part_doubles = (size_t)2 * c->sms * 4;
+    c->metrics.ensure((part_doubles + 8) * sizeof(double));
+    double* out2 = c->metrics.d() + part_doubles;
+    DBuf dr;
+    dr.ensure((size_t)m * m * sizeof(double));
+    CUDA_OK(cudaMemcpy2DAsync(dr.p, m * sizeof(double), h_r, ldr * sizeof(double), m * sizeof(double),
+                              m, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(residual_launch(d_x, ldx, d_q, ldq, dr.d(), m, n_local, m, 1.0, 1.0, c->metrics.d(),
+                            out2, c->sms, c->stream));
+    if (c->nranks > 1)
+      NCCL_OK(nccl().AllReduce(out2, out2, 2, ncclDouble, ncclSum, c->comm, c->stream));
+    double h[2];
+    CUDA_OK(cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    dr.release();
+    if (resid) *resid = h[1] == 0.0 ? std::sqrt(h[0]) : std::sqrt(h[0]) / std::sqrt(h[1]);
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_metrics(bgs_ctx* c, long n, long m, const double* x, long ldx, const double* q, long ldq,
+                const double* r, long ldr, double* loo, double* resid, bgs_error* err) {
+  clear_err(err);
+  try {
+    select_device(c);
+    if (n < 1 || m < 1 || ldx < n || ldq < n || ldr < m) fail(BGS_E_DIMENSION, "bgs_metrics: shape");
+    const long ld = even_ld(n);
+    DBuf dx, dq;
+    dx.ensure((size_t)ld * m * sizeof(double));
+    dq.ensure((size_t)ld * m * sizeof(double));
+    CUDA_OK(cudaMemcpy2DAsync(dx.p, ld * sizeof(double), x, ldx * sizeof(double), n * sizeof(double),
+                              m, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpy2DAsync(dq.p, ld * sizeof(double), q, ldq * sizeof(double), n * sizeof(double),
+                              m, cudaMemcpyHostToDevice, c->stream));
+    const int rc = bgs_metrics_device(c, n, m, n, dx.d(), ld, dq.d(), ld, r, ldr, loo, resid, err);
+    dx.release();
+    dq.release();
+    return rc;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_gram(bgs_ctx* c, const double* a, long n, long ma, const double* b, long mb, double* out,
+             bgs_error* err) {
+  clear_err(err);
+  try {
+    select_device(c);
+    if (n < 1 || ma < 1 || mb < 1 || mb > 32 || ma > 4096) fail(BGS_E_DIMENSION, "bgs_gram: shape");
+    const long ld = even_ld(n);
+    DBuf da, db;
+    da.ensure((size_t)ld * ma * sizeof(double));
+    db.ensure((size_t)ld * mb * sizeof(double));
+    CUDA_OK(cudaMemcpy2DAsync(da.p, ld * sizeof(double), a, n * sizeof(double), n * sizeof(double), ma,
+                              cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpy2DAsync(db.p, ld * sizeof(double), b, n * sizeof(double), n * sizeof(double), mb,
+                              cudaMemcpyHostToDevice, c->stream));
+    Runner run(c, BGS_BCGSI_PLUS_P_1S, n, std::max(ma, mb), 1, 1, false, nullptr);
+    Shard sh;
+    sh.rows = n;
+    sh.Q = da.d(); sh.ldq = ld;
+    sh.X = db.d(); sh.ldx = ld;
+    sh.mapQ = make_map(da.d(), n, ma, ld);
+    sh.mapX = make_map(db.d(), n, mb, ld);
+    run.sh.push_back(sh);
+    c->status.ensure(sizeof(DevStatus));
+    run.status = reinterpret_cast<DevStatus*>(c->status.p);
+    CUDA_OK(cudaMemsetAsync(run.status, 0, sizeof(DevStatus), c->stream));
+    const size_t per_cta = gram_partial_doubles_per_cta((int)((ma + 7) / 8), (int)mb);
+    c->partial.ensure(per_cta * sizeof(double) * (size_t)run.grid_total() + 64);
+    c->G.ensure((size_t)ma * mb * sizeof(double) + 64);
+    GramSpec g = Runner::spec2(SQ, 0, (int)ma, (int)ma, SX, 0, (int)mb, 0);
+    run.set_right(g, 1, 0, (int)mb);
+    run.gram(g, "", false, false);
+    CUDA_OK(cudaMemcpyAsync(out, c->G.p, (size_t)ma * mb * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    da.release();
+    db.release();
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_tsqr(bgs_ctx* c, const double* x, long n, long s, double* q, double* r, bgs_error* err) {
+  clear_err(err);
+  try {
+    select_device(c);
+    if (s < 1 || s > 16) fail(BGS_E_CONFIG, "bgs_tsqr: 1 <= s <= 16");
+    if (n < s) fail(BGS_E_RANK_DEFICIENT, "tsqr: block has %ld columns but only %ld global rows", s, n);
+    const long ld = even_ld(n);
+    DBuf dx, dq;
+    dx.ensure((size_t)ld * s * sizeof(double));
+    dq.ensure((size_t)ld * s * sizeof(double));
+    CUDA_OK(cudaMemcpy2DAsync(dx.p, ld * sizeof(double), x, n * sizeof(double), n * sizeof(double), s,
+                              cudaMemcpyHostToDevice, c->stream));
+    Runner run(c, BGS_BCGSI_PLUS, n, s, s, 1, false, nullptr);
+    Shard sh;
+    sh.rows = n;
+    sh.X = dx.d(); sh.ldx = ld;
+    sh.Q = dq.d(); sh.ldq = ld;
+    run.sh.push_back(sh);
+    run.setup();
+    run.tsqr(SX, 0, 0, c->rtop.d(), (int)s, "reduce_factor_tree:tsqr");
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpy2D(q, n * sizeof(double), dq.p, ld * sizeof(double), n * sizeof(double), s,
+                         cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(r, c->rtop.p, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToHost));
+    dx.release();
+    dq.release();
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,442 @@
+// tsqr.cu — K4: communication-avoiding TSQR of a tall n x s block on the device.
+//
+// Replaces run_tsqr / factor_local_leaves / plan_leaves (intraorth.cpp:27-111),
+// householder_qr (dense_kernels.cpp:135-203), combine_leaf_factors / propagate_tree
+// (tsqr_tree.cpp:14-78) and the tree half of tsqr_leaf_reduce (communicator.cpp:252-317).
+//
+//  leaf kernel : one CTA per row leaf (<= 1024 rows); Householder QR in shared memory with
+//                the reference's scaled-norm reflector and nonnegative-diagonal sign fix;
+//                writes the explicit leaf Q in place and the leaf R (s x s).
+//  up kernel   : one CTA per shard tree; levels of pairwise QRs of stacked 2s x s R
+//                factors, one warp per pair (lanes = rows); node Q factors kept.
+//  cross kernel: the tree over the per-rank roots (after an NCCL allgather on a
+//                multi-GPU context); identical inputs -> bitwise identical on every rank.
+//  down kernel : pushes the root's M down the tree: M_leaf with Q_global = Q_leaf M_leaf.
+//  apply kernel: Q rows of each leaf <- Q rows * M_leaf.
+// Every factor is carried as s x s (zero-padded rows for short leaves, which stack as
+// no-ops exactly like the reference's trapezoidal factors).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bgs {
+
+namespace {
+
+constexpr int SMAX = 16;
+constexpr int kLeafThreads = 256;
+
+// ---------------------------------------------------------------------------------
+// CTA reductions (deterministic order)
+// ---------------------------------------------------------------------------------
+__device__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sums nv (<= SMAX) per-thread values over the CTA; result broadcast in out[0..nv).
+__device__ void cta_sum_multi(double* v, int nv, double* scratch /*[8][SMAX]*/, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = 0; i < nv; ++i) {
+    const double r = warp_sum(v[i]);
+    if (lane == 0) scratch[warp * SMAX + i] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double acc = 0.0;
+    for (int w = 0; w < kLeafThreads / 32; ++w) acc += scratch[w * SMAX + threadIdx.x];
+    out[threadIdx.x] = acc;
+  }
+  __syncthreads();
+}
+
+__device__ double cta_max(double v, double* scratch, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double r = warp_max(v);
+  if (lane == 0) scratch[warp] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < kLeafThreads / 32; ++w) m = fmax(m, scratch[w]);
+    out[0] = m;
+  }
+  __syncthreads();
+  return out[0];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+// Leaf Householder QR
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kLeafThreads)
+    tsqr_leaf_kernel(const double* __restrict__ src, long lds, double* __restrict__ dst,
+                     long ldd, const long* __restrict__ leaf_row0, int s,
+                     double* __restrict__ rleaf, const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  extern __shared__ __align__(16) double sm[];
+  const int l = blockIdx.x;
+  const long g0 = leaf_row0[l];
+  const int h = (int)(leaf_row0[l + 1] - g0);
+  double* A = sm;                    // h x s (V below the diagonal after the sweep)
+  double* Q = A + (size_t)h * s;     // h x s
+  __shared__ double scratch[8 * SMAX];
+  __shared__ double red[SMAX];
+  __shared__ double v0s[SMAX], taus[SMAX], rdiag[SMAX], rup[SMAX * SMAX];
+  const int tid = threadIdx.x;
+  const int p = h < s ? h : s;
+
+  for (int j = 0; j < s; ++j)
+    for (int i = tid; i < h; i += kLeafThreads) A[i + j * h] = src[g0 + i + (size_t)j * lds];
+  __syncthreads();
+
+  for (int k = 0; k < p; ++k) {
+    double lm = 0.0;
+    for (int i = k + tid; i < h; i += kLeafThreads) lm = fmax(lm, fabs(A[i + k * h]));
+    const double mx = cta_max(lm, scratch, red);
+    if (mx == 0.0) {
+      if (tid == 0) { taus[k] = 0.0; v0s[k] = 0.0; rdiag[k] = A[k + k * h]; }
+      __syncthreads();
+      continue;
+    }
+    // scaled sum of squares of a(k:h, k) and plain sum of squares of a(k+1:h, k)
+    double v2[2] = {0.0, 0.0};
+    for (int i = k + tid; i < h; i += kLeafThreads) {
+      const double a = A[i + k * h];
+      const double t = a / mx;
+      v2[0] = fma(t, t, v2[0]);
+      if (i > k) v2[1] = fma(a, a, v2[1]);
+    }
+    cta_sum_multi(v2, 2, scratch, red);
+    const double sigma = mx * sqrt(red[0]);
+    const double akk = A[k + k * h];
+    const double alpha = akk >= 0.0 ? -sigma : sigma;
+    const double v0 = akk - alpha;
+    const double vtv = v0 * v0 + red[1];
+    const double tau = vtv == 0.0 ? 0.0 : 2.0 / vtv;
+    // w_j = tau * (v0 a(k,j) + sum_{i>k} v_i a(i,j)),  j > k
+    double w[SMAX];
+    const int nj = s - k - 1;
+    for (int j = 0; j < nj; ++j) w[j] = 0.0;
+    for (int i = k + 1 + tid; i < h; i += kLeafThreads) {
+      const double vi = A[i + k * h];
+      for (int j = 0; j < nj; ++j) w[j] = fma(vi, A[i + (k + 1 + j) * h], w[j]);
+    }
+    __syncthreads();
+    cta_sum_multi(w, nj, scratch, red);
+    for (int j = 0; j < nj; ++j) {
+      const double wj = tau * fma(v0, A[k + (k + 1 + j) * h], red[j]);
+      for (int i = k + 1 + tid; i < h; i += kLeafThreads)
+        A[i + (k + 1 + j) * h] -= wj * A[i + k * h];
+      w[j] = wj;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < nj; ++j) A[k + (k + 1 + j) * h] -= w[j] * v0;
+      v0s[k] = v0;
+      taus[k] = tau;
+      rdiag[k] = alpha;
+    }
+    __syncthreads();
+  }
+  // R (s x s, zero padded) before the sign fix
+  if (tid < s * s) {
+    const int i = tid % s, j = tid / s;
+    double v = 0.0;
+    if (i < p && i <= j) v = (i == j) ? rdiag[i] : A[i + j * h];
+    rup[tid] = v;
+  }
+  // Q = H_0 ... H_{p-1} [I; 0]
+  for (int j = 0; j < s; ++j)
+    for (int i = tid; i < h; i += kLeafThreads) Q[i + j * h] = (i == j && j < p) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int k = p - 1; k >= 0; --k) {
+    const double tau = taus[k];
+    if (tau == 0.0) continue;
+    const double v0 = v0s[k];
+    double w[SMAX];
+    for (int j = 0; j < p; ++j) w[j] = 0.0;
+    for (int i = k + 1 + tid; i < h; i += kLeafThreads) {
+      const double vi = A[i + k * h];
+      for (int j = 0; j < p; ++j) w[j] = fma(vi, Q[i + j * h], w[j]);
+    }
+    cta_sum_multi(w, p, scratch, red);
+    for (int j = 0; j < p; ++j) w[j] = tau * fma(v0, Q[k + j * h], red[j]);
+    for (int i = k + 1 + tid; i < h; i += kLeafThreads) {
+      const double vi = A[i + k * h];
+      for (int j = 0; j < p; ++j) Q[i + j * h] -= w[j] * vi;
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int j = 0; j < p; ++j) Q[k + j * h] -= w[j] * v0;
+    __syncthreads();
+  }
+  // canonical sign: nonnegative diag(R)
+  __shared__ double sgn[SMAX];
+  if (tid < s) sgn[tid] = (tid < p && rup[tid + tid * s] < 0.0) ? -1.0 : 1.0;
+  __syncthreads();
+  if (tid < s * s) {
+    const int i = tid % s;
+    rleaf[(size_t)l * s * s + tid] = sgn[i] * rup[tid];
+  }
+  for (int j = 0; j < s; ++j)
+    for (int i = tid; i < h; i += kLeafThreads) dst[g0 + i + (size_t)j * ldd] = sgn[j] * Q[i + j * h];
+}
+
+// ---------------------------------------------------------------------------------
+// Pairwise QR of two stacked s x s factors, one warp: lane i < 2s owns row i.
+// q (2s x s, col-major) and r (s x s) written to global/shared.
+// ---------------------------------------------------------------------------------
+__device__ void warp_pair_qr(const double* top, const double* bot, int s, double* qout,
+                             double* rout) {
+  const int lane = threadIdx.x & 31;
+  const int m = 2 * s;
+  double a[SMAX];
+  for (int j = 0; j < s; ++j)
+    a[j] = lane < s ? top[lane + j * s] : (lane < m ? bot[(lane - s) + j * s] : 0.0);
+  double vs[SMAX], taus[SMAX], rd[SMAX];
+  for (int k = 0; k < s; ++k) {
+    const double mine = (lane >= k && lane < m) ? a[k] : 0.0;
+    const double mx = warp_max(fabs(mine));
+    if (mx == 0.0) {
+      taus[k] = 0.0; vs[k] = 0.0;
+      rd[k] = __shfl_sync(0xffffffffu, a[k], k);
+      continue;
+    }
+    const double t = mine / mx;
+    const double ssq = warp_sum(t * t);
+    const double below = warp_sum(lane > k ? mine * mine : 0.0);
+    const double sigma = mx * sqrt(ssq);
+    const double akk = __shfl_sync(0xffffffffu, a[k], k);
+    const double alpha = akk >= 0.0 ? -sigma : sigma;
+    const double v0 = akk - alpha;
+    const double vtv = v0 * v0 + below;
+    const double tau = vtv == 0.0 ? 0.0 : 2.0 / vtv;
+    const double vi = lane == k ? v0 : (lane > k && lane < m ? a[k] : 0.0);
+    for (int j = k + 1; j < s; ++j) {
+      const double wj = tau * warp_sum(vi * a[j]);
+      a[j] -= wj * vi;
+    }
+    vs[k] = vi;
+    taus[k] = tau;
+    rd[k] = alpha;
+  }
+  // R rows (lane i < s): a[j] for j > i, rd[i] on the diagonal
+  double q[SMAX];
+  for (int j = 0; j < s; ++j) q[j] = (lane == j) ? 1.0 : 0.0;
+  for (int k = s - 1; k >= 0; --k) {
+    if (taus[k] == 0.0) continue;
+    for (int j = 0; j < s; ++j) {
+      const double wj = taus[k] * warp_sum(vs[k] * q[j]);
+      q[j] -= wj * vs[k];
+    }
+  }
+  // sign fix: lane j knows whether R(j,j) < 0
+  for (int j = 0; j < s; ++j) {
+    const double d = rd[j];
+    const double sg = d < 0.0 ? -1.0 : 1.0;
+    if (lane < m) qout[lane + j * m] = sg * q[j];
+    if (lane == j) {
+      for (int jj = 0; jj < s; ++jj) {
+        double v = 0.0;
+        if (jj == j) v = d;
+        else if (jj > j) v = a[jj];
+        rout[j + jj * s] = sg * v;
+      }
+    } else if (lane > j && lane < s) {
+      rout[lane + j * s] = 0.0;
+    }
+  }
+}
+
+// C = A(s x s, lda) * B(s x s); one warp.
+__device__ void warp_mm(const double* A, int lda, const double* B, int s, double* C) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < s * s; e += 32) {
+    const int i = e % s, j = e / s;
+    double acc = 0.0;
+    for (int k = 0; k < s; ++k) acc = fma(A[i + k * lda], B[k + j * s], acc);
+    C[e] = acc;
+  }
+}
+
+// Workspace layout per leaf index: [R | Rtmp | M | Mtmp] (s*s each) + nodeQ (2s*s)
+struct TreeWs {
+  double *R, *Rt, *M, *Mt, *NQ;
+};
+__device__ TreeWs tree_ws(double* ws, int L, int s) {
+  const size_t ss = (size_t)s * s;
+  TreeWs t;
+  t.R = ws;
+  t.Rt = ws + L * ss;
+  t.M = ws + 2 * L * ss;
+  t.Mt = ws + 3 * L * ss;
+  t.NQ = ws + 4 * L * ss;
+  return t;
+}
+
+// Bottom-up over items [off, off + c) of the workspace; root -> root_out (ld lr).
+__device__ void tree_up(TreeWs w, int off, int c, int s, double* root_out, int lr) {
+  const size_t ss = (size_t)s * s;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* cur = w.R + off * ss;
+  double* nxt = w.Rt + off * ss;
+  int node = off;
+  int cnt = c;
+  while (cnt > 1) {
+    const int np = cnt / 2;
+    for (int i = warp; i < np; i += nw)
+      warp_pair_qr(cur + 2 * i * ss, cur + (2 * i + 1) * ss, s, w.NQ + (size_t)(node + i) * 2 * ss,
+                   nxt + i * ss);
+    if (cnt & 1)
+      for (int e = threadIdx.x; e < (int)ss; e += blockDim.x) nxt[np * ss + e] = cur[(cnt - 1) * ss + e];
+    __syncthreads();
+    node += np;
+    cnt = np + (cnt & 1);
+    double* t = cur; cur = nxt; nxt = t;
+  }
+  for (int e = threadIdx.x; e < (int)ss; e += blockDim.x) root_out[(e % s) + (e / s) * lr] = cur[e];
+  __syncthreads();
+}
+
+// Top-down: leaf M's into w.M[off .. off+c)
+__device__ void tree_down(TreeWs w, int off, int c, int s, const double* mtop) {
+  const size_t ss = (size_t)s * s;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int cnts[40], bases[40];
+  int nl = 0, cnt = c, node = off;
+  while (cnt > 1) {
+    cnts[nl] = cnt;
+    bases[nl] = node;
+    node += cnt / 2;
+    cnt = cnt / 2 + (cnt & 1);
+    ++nl;
+  }
+  // the buffer that must end up holding level 0 is w.M; alternate backwards
+  double* bufs[2] = {w.M + off * ss, w.Mt + off * ss};
+  int top_buf = nl & 1;  // level l lives in bufs[l & 1]; level nl (root) in bufs[nl & 1]
+  double* root = bufs[top_buf];
+  for (int e = threadIdx.x; e < (int)ss; e += blockDim.x)
+    root[e] = mtop ? mtop[e] : ((e % s) == (e / s) ? 1.0 : 0.0);
+  __syncthreads();
+  for (int lv = nl - 1; lv >= 0; --lv) {
+    double* par = bufs[(lv + 1) & 1];
+    double* chi = bufs[lv & 1];
+    const int cn = cnts[lv], np = cn / 2;
+    for (int i = warp; i < np; i += nw) {
+      const double* qn = w.NQ + (size_t)(bases[lv] + i) * 2 * ss;
+      warp_mm(qn, 2 * s, par + i * ss, s, chi + 2 * i * ss);
+      warp_mm(qn + s, 2 * s, par + i * ss, s, chi + (2 * i + 1) * ss);
+    }
+    if (cn & 1)
+      for (int e = threadIdx.x; e < (int)ss; e += blockDim.x) chi[(cn - 1) * ss + e] = par[np * ss + e];
+    __syncthreads();
+  }
+}
+
+__global__ void tsqr_up_kernel(const int* tree_off, double* ws, int L, int s, double* roots,
+                               const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  const int t = blockIdx.x;
+  const int off = tree_off[t], c = tree_off[t + 1] - tree_off[t];
+  tree_up(tree_ws(ws, L, s), off, c, s, roots + (size_t)t * s * s, s);
+}
+
+__global__ void tsqr_down_kernel(const int* tree_off, double* ws, int L, int s,
+                                 const double* mtop, const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  const int t = blockIdx.x;
+  const int off = tree_off[t], c = tree_off[t + 1] - tree_off[t];
+  tree_down(tree_ws(ws, L, s), off, c, s, mtop ? mtop + (size_t)t * s * s : nullptr);
+}
+
+__global__ void tsqr_cross_kernel(const double* roots, int n, int s, double* ws2, double* rout,
+                                  int ldr, double* mout, const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  TreeWs w = tree_ws(ws2, n, s);
+  const size_t ss = (size_t)s * s;
+  for (int e = threadIdx.x; e < (int)(n * ss); e += blockDim.x) w.R[e] = roots[e];
+  __syncthreads();
+  tree_up(w, 0, n, s, rout, ldr);
+  if (mout) {
+    tree_down(w, 0, n, s, nullptr);
+    for (int e = threadIdx.x; e < (int)(n * ss); e += blockDim.x) mout[e] = w.M[e];
+  }
+}
+
+__global__ void tsqr_apply_kernel(double* dst, long ldd, const long* leaf_row0, const double* M,
+                                  int s, const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  __shared__ double m[SMAX * SMAX];
+  const int l = blockIdx.x;
+  for (int e = threadIdx.x; e < s * s; e += blockDim.x) m[e] = M[(size_t)l * s * s + e];
+  __syncthreads();
+  const long g0 = leaf_row0[l], g1 = leaf_row0[l + 1];
+  for (long i = g0 + threadIdx.x; i < g1; i += blockDim.x) {
+    double row[SMAX];
+    for (int j = 0; j < s; ++j) row[j] = dst[i + (size_t)j * ldd];
+    for (int j = 0; j < s; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < s; ++k) acc = fma(row[k], m[k + j * s], acc);
+      dst[i + (size_t)j * ldd] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------------
+size_t tsqr_ws_bytes(int leaves, int s) {
+  return (size_t)leaves * s * s * 6 * sizeof(double);
+}
+
+cudaError_t tsqr_leaf_launch(const double* src, long lds, double* dst, long ldd,
+                             const long* d_bounds, int L, long hmax, int s, double* rleaf,
+                             const DevStatus* status, cudaStream_t st, int* launches) {
+  const size_t smem = (size_t)2 * (hmax > 0 ? hmax : 1) * s * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(tsqr_leaf_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  tsqr_leaf_kernel<<<L, kLeafThreads, smem, st>>>(src, lds, dst, ldd, d_bounds, s, rleaf, status);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t tsqr_up_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
+                           double* roots, const DevStatus* status, cudaStream_t st,
+                           int* launches) {
+  tsqr_up_kernel<<<n_trees, 512, 0, st>>>(d_tree_off, ws, L, s, roots, status);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t tsqr_down_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
+                             const double* mtop, const DevStatus* status, cudaStream_t st,
+                             int* launches) {
+  tsqr_down_kernel<<<n_trees, 512, 0, st>>>(d_tree_off, ws, L, s, mtop, status);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t tsqr_apply_launch(double* dst, long ldd, const long* d_bounds, int L, int s,
+                              const double* M, const DevStatus* status, cudaStream_t st,
+                              int* launches) {
+  tsqr_apply_kernel<<<L, 256, 0, st>>>(dst, ldd, d_bounds, M, s, status);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t tsqr_cross_launch(const double* roots, int n, int s, double* ws2, double* rout,
+                              int ldrout, double* mout, const DevStatus* status,
+                              cudaStream_t st, int* launches) {
+  tsqr_cross_kernel<<<1, 512, 0, st>>>(roots, n, s, ws2, rout, ldrout, mout, status);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace bgs

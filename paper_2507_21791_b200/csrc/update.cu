@@ -1,0 +1,190 @@
+// update.cu — K2: fused tall-skinny block update.
+//
+// Replaces local_axpy_block (dist_block.cpp:90-108) + scale_right_block /
+// tri_solve_right (dist_block.cpp:110-117, dense_kernels.cpp:89-110) + the
+// extract_block / set_block copies (dist_block.cpp:46-49, 119-125) of one block step of
+// bcgs.cpp.  One pass over the Q prefix produces up to two output blocks per row:
+//
+//   A = (srcA - Qp * CA) * TA^{-1}                       (e.g. Q_k = (U - Q Y) Y_kk^{-1})
+//   B = (srcB - Qp * CB[0:kp] - A * CB[kp:kp+s]) * TB^{-1}
+//                                   (e.g. U_{k+1} = (X_{k+1} - Q_{1:k+1} [Z; S2]) S^{-1})
+//
+// Triangular factors are applied by back-substitution (never an explicit inverse,
+// SPEC.md:383/415), exactly as tri_solve_right does per row.  Each thread owns RPT
+// consecutive rows; the prefix columns are read once, coalesced, with 128-bit loads;
+// the (kp x 2s) coefficient panel is staged in shared memory and read as broadcasts.
+// HBM traffic per row: 8*(kp + 2s) bytes read + 8*2s written.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bgs {
+
+template <int S, int RPT, bool HA, bool HB>
+__global__ void __launch_bounds__(256) update_kernel(const UpdateParams p) {
+  if (p.status && status_bad(p.status)) return;
+  extern __shared__ __align__(16) double coef[];  // [kp][2S] interleaved CA | CB rows
+  double* ta = coef + (size_t)p.kp * 2 * S;        // S x S (col-major)
+  double* tb = ta + S * S;                         // S x S
+  double* cbx = tb + S * S;                        // S x S: CB rows kp..kp+S-1
+  const int kp = p.kp;
+  // Runtime block width s <= S: padded coefficient columns are zero and padded
+  // triangular factors are the identity, so padded outputs are exact zeros (not stored).
+  const int s = p.s;
+  for (int idx = threadIdx.x; idx < kp * S; idx += blockDim.x) {
+    const int c = idx / S, j = idx % S;
+    coef[c * 2 * S + j] = (HA && j < s) ? p.CA[c + (size_t)j * p.ldca] : 0.0;
+    coef[c * 2 * S + S + j] = (HB && j < s) ? p.CB[c + (size_t)j * p.ldcb] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {
+    const int i = idx % S, j = idx / S;
+    const bool in = i < s && j < s;
+    ta[idx] = (HA && p.TA && in) ? p.TA[i + (size_t)j * p.ldta] : (i == j ? 1.0 : 0.0);
+    tb[idx] = (HB && p.TB && in) ? p.TB[i + (size_t)j * p.ldtb] : (i == j ? 1.0 : 0.0);
+    cbx[idx] = (HA && HB && p.cb_has_a && in) ? p.CB[kp + i + (size_t)j * p.ldcb] : 0.0;
+  }
+  __syncthreads();
+
+  const long nrow_groups = (p.n_rows + RPT - 1) / RPT;
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < nrow_groups;
+       g += (long)gridDim.x * blockDim.x) {
+    const long r0 = g * RPT;
+    double accA[RPT][S], accB[RPT][S];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int j = 0; j < S; ++j) accA[r][j] = accB[r][j] = 0.0;
+
+    const double* qcol = p.qp + r0;
+    int c = 0;
+    // 4-way unrolled stream over the prefix columns (independent loads in flight).
+    for (; c + 4 <= kp; c += 4) {
+      double v[4][RPT];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* ptr = qcol + (size_t)(c + u) * p.ldq;
+        if (RPT == 2) {
+          const double2 t = __ldg(reinterpret_cast<const double2*>(ptr));
+          v[u][0] = t.x;
+          v[u][RPT - 1] = t.y;
+        } else {
+          v[u][0] = __ldg(ptr);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* cr = coef + (c + u) * 2 * S;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const double ca = cr[j], cb = cr[S + j];
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            if (HA) accA[r][j] = fma(v[u][r], ca, accA[r][j]);
+            if (HB) accB[r][j] = fma(v[u][r], cb, accB[r][j]);
+          }
+        }
+      }
+    }
+    for (; c < kp; ++c) {
+      double v[RPT];
+      const double* ptr = qcol + (size_t)c * p.ldq;
+      if (RPT == 2) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(ptr));
+        v[0] = t.x;
+        v[RPT - 1] = t.y;
+      } else {
+        v[0] = __ldg(ptr);
+      }
+      const double* cr = coef + c * 2 * S;
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          if (HA) accA[r][j] = fma(v[r], cr[j], accA[r][j]);
+          if (HB) accB[r][j] = fma(v[r], cr[S + j], accB[r][j]);
+        }
+    }
+
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const long row = r0 + r;
+      if (row >= p.n_rows) break;
+      double a[S];
+      if (HA) {
+        // A = (srcA - acc) * TA^{-1}: back-substitution along the row (tri_solve_right)
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          double t = (j < s ? p.srcA[row + (size_t)j * p.ld_srcA] : 0.0) - accA[r][j];
+#pragma unroll
+          for (int l = 0; l < j; ++l) t -= a[l] * ta[l + j * S];
+          a[j] = t / ta[j + j * S];
+        }
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j < s) p.dstA[row + (size_t)j * p.ld_dstA] = a[j];
+      }
+      if (HB) {
+        double b[S];
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          double t = (j < s ? p.srcB[row + (size_t)j * p.ld_srcB] : 0.0) - accB[r][j];
+          if (HA && p.cb_has_a) {
+#pragma unroll
+            for (int l = 0; l < S; ++l) t -= a[l] * cbx[l + j * S];
+          }
+#pragma unroll
+          for (int l = 0; l < j; ++l) t -= b[l] * tb[l + j * S];
+          b[j] = t / tb[j + j * S];
+        }
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j < s) p.dstB[row + (size_t)j * p.ld_dstB] = b[j];
+      }
+    }
+  }
+}
+
+template <int S, int RPT>
+static cudaError_t launch_s(const UpdateParams& p, int grid, size_t smem, cudaStream_t st) {
+  const bool ha = p.has_a, hb = p.has_b;
+  if (ha && hb) {
+    auto k = update_kernel<S, RPT, true, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 256, smem, st>>>(p);
+  } else if (ha) {
+    auto k = update_kernel<S, RPT, true, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 256, smem, st>>>(p);
+  } else if (hb) {
+    auto k = update_kernel<S, RPT, false, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 256, smem, st>>>(p);
+  } else {
+    return cudaSuccess;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t update_launch(const UpdateParams& p, int num_sms, cudaStream_t st, int* launches) {
+  const int s = p.s;
+  const int S = s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : s <= 8 ? 8 : 16;
+  if (s < 1 || s > 16) return cudaErrorInvalidValue;
+  const size_t smem = ((size_t)p.kp * 2 * S + 3 * S * S) * sizeof(double) + 16;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const int rpt = S <= 4 ? 2 : 1;
+  const long groups = (p.n_rows + rpt - 1) / rpt;
+  long grid = (groups + 255) / 256;
+  const long cap = (long)num_sms * (smem > 64 * 1024 ? 2 : 4);
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  if (launches) *launches += 1;
+  switch (S) {
+    case 1: return launch_s<1, 2>(p, (int)grid, smem, st);
+    case 2: return launch_s<2, 2>(p, (int)grid, smem, st);
+    case 4: return launch_s<4, 2>(p, (int)grid, smem, st);
+    case 8: return launch_s<8, 1>(p, (int)grid, smem, st);
+    case 16: return launch_s<16, 1>(p, (int)grid, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace bgs
