@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 BCGSI+P-1S QR on B200 (BASELINE.json metric / config 2).
+
+One "step" = one full factorization X -> (Q, R) of the workload (default BASELINE
+config 2: n=1e6, m=400, s=4, i.i.d. N(0,1)), rows sharded over the ranks, X resident in
+HBM when the timed region starts.  `value` = whole-job fp64 GFLOP/s, the reference's own
+analytic flop count (variant_flops, cost_model.cpp:29-119) / device time (max over ranks).
+
+    python bench.py [--gpus N --steps K --warmup W]          # our B200 path
+    python bench.py --impl reference [...]                   # the reference CPU path
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+VARIANT_DEFAULT = "BCGSI+P-1S"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default=VARIANT_DEFAULT)
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--m", type=int, default=400)
+    ap.add_argument("--s", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU seconds of one reference sample run")
+    return ap.parse_args()
+
+
+def workload_config(a, world):
+    return {
+        "workload": f"{a.variant} n={a.n} m={a.m} s={a.s} fp64 i.i.d. N(0,1) "
+                    f"(BASELINE.json config 2)",
+        "variant": a.variant, "n": a.n, "m": a.m, "s": a.s, "seed": a.seed,
+        "parallelism": f"row-sharded dp{world} (1-D ceil split), 1 allreduce per block step",
+        "l2": f"inputs exceed L2: X is {a.n * a.m * 8 / 1e9:.2f} GB (126 MB L2), no flush needed",
+    }
+
+
+def metric_name(a):
+    return f"fp64 QR time & GFLOP/s, {a.variant} n={a.n:.0e} m={a.m} s={a.s}".replace("+0", "")
+
+
+# ---------------------------------------------------------------------------------------
+# CPU reference (test-infrastructure checker, timed on the host cores)
+# ---------------------------------------------------------------------------------------
+def cpu_reference_runner(v, n, m, s, seed):
+    """Returns (kind, run(n_rows) -> (seconds, flops))."""
+    from oracle.oracle import Oracle, Reference
+    cores = os.cpu_count() or 1
+    if Reference.available():
+        ref = Reference()
+        kind = "reference"
+
+        def run(rows):
+            x = ref.gen_matrix(rows, m, s, 1.0, seed, True)
+            res = ref.factor(v, x, s, procs=cores, want_q=False)
+            return res.seconds
+    else:
+        ref = Oracle()
+        kind = "port"
+        cores = int(os.environ.get("OMP_NUM_THREADS", cores))
+
+        def run(rows):
+            x = ref.gen_matrix(rows, m, s, 1.0, seed, True)
+            t = time.perf_counter()
+            ref.factor(v, x, s, 1)
+            return time.perf_counter() - t
+    return kind, cores, run
+
+
+def pick_sample_rows(run, n, m, target_s):
+    rows = max(m, 1000)
+    t = run(rows)
+    want = int(rows * target_s / max(t, 1e-3))
+    return max(m, min(n, want)), t
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel):
+    """dram bytes per launch / algorithmic bytes per launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------------------
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    import paper_2507_21791_b200 as bgs
+    v = bgs.parse_variant(a.variant)
+    per_step = max(2.0, a.cpu_seconds * 8.0 / max(8, a.steps + a.warmup))
+    kind, cores, run = cpu_reference_runner(int(v), a.n, a.m, a.s, a.seed)
+    rows, _ = pick_sample_rows(run, a.n, a.m, per_step)
+    for _ in range(a.warmup):
+        run(rows)
+    secs = [run(rows) for _ in range(a.steps)]
+    t = sum(secs) / len(secs)
+    flops = bgs.variant_flops(int(v), rows, a.m, a.s)
+    gf = flops / t / 1e9
+    sample = (f"{a.variant} n={rows} m={a.m} s={a.s} N(0,1) (row subsample of the workload; "
+              f"cost and flops both scale with n), {'reference library oracle/_ref' if kind == 'reference' else 'oracle port'} "
+              f"run_variant under run_spmd with P={cores} threads, mean of {a.steps} runs")
+    line = {
+        "impl": "reference", "metric": metric_name(a), "value": gf, "unit": "GFLOP/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": t * 1e3 * (a.n / rows), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), reference gen_matrix)",
+        "config": workload_config(a, world),
+        "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "ms_per_step extrapolated to the full n from the sample (cost is linear in n)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_21791_b200 as bgs
+    from paper_2507_21791_b200 import api
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus if a.gpus == 1 else 1)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    uid = None
+    if world > 1:
+        obj = [bgs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = bgs.Context(local, rank, world, uid)
+    v = int(bgs.parse_variant(a.variant))
+    n, m, s = a.n, a.m, a.s
+    row0, nl = bgs.shard_rows(n, world, rank)
+    ld = max(2, (nl + 1) // 2 * 2)
+    X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
+    Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    bgs.gen_gaussian_device(ctx, a.seed, row0, nl, m, X.data_ptr(), ld)
+    torch.cuda.synchronize()
+    flops = bgs.variant_flops(v, n, m, s)
+
+    def step():
+        return bgs.factor_device(ctx, v, n, m, s, row0, nl, X.data_ptr(), ld, Q.data_ptr(), ld)
+
+    for _ in range(a.warmup):
+        r, st, tm = step()
+    ctx.read_profile()  # drop warm-up samples
+    ctx.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    ms_list, launches = [], 0
+    with ClockSampler(local) as cs:
+        t_wall = time.perf_counter()
+        for _ in range(a.steps):
+            r, st, tm = step()
+            ms_list.append(tm.factor_ms)
+            launches += tm.kernel_launches
+        torch.cuda.synchronize()
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    ctx.profile(False)
+    prof = ctx.read_profile()
+    ms = allmax(sum(ms_list) / len(ms_list))
+    value = flops / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (live CUDA events over the timed region) ----
+    peak, peak_src = hbm_peak()
+    dom = max((k for k in prof if k in ("gram", "update")), key=lambda k: prof[k]["ms"],
+              default=None)
+    roof = None
+    kern = {}
+    total_ms = sum(p["ms"] for p in prof.values())
+    for k, p in prof.items():
+        kern[k] = {"launches": p["launches"], "ms_total": p["ms"],
+                   "share": p["ms"] / total_ms if total_ms else None,
+                   "gbs": (p["alg_bytes"] / p["ms"] / 1e6) if p["ms"] and p["alg_bytes"] else None}
+    if dom:
+        p = prof[dom]
+        ach = p["alg_bytes"] / p["ms"] / 1e6
+        tr = ncu_traffic(dom)
+        per_launch = p["alg_bytes"] / max(1, p["launches"])
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": (tr * per_launch) if tr else None, "kernel": dom,
+                "peak_source": peak_src,
+                "alg_bytes_per_launch": per_launch,
+                "avg_launch_ms": p["ms"] / max(1, p["launches"])}
+    # whole-factorization roofline: algorithmic bytes of all kernels / step time
+    step_bytes = sum(p["alg_bytes"] for p in prof.values()) / a.steps
+
+    # ---- verification at full size (untimed): LOO and residual on the device ----
+    verify = None
+    if not a.no_verify:
+        loo, res = bgs.metrics_device(ctx, n, m, nl, X.data_ptr(), ld, Q.data_ptr(), ld, r)
+        verify = {"loo": loo, "resid": res, "sync_count": st.sync_count,
+                  "expected_syncs": bgs.expected_syncs(v, m // s),
+                  "words_reduced": st.words_reduced}
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not a.no_e2e:
+        hx = torch.empty((m, nl), dtype=torch.float64, pin_memory=True)
+        hq = torch.empty((m, nl), dtype=torch.float64, pin_memory=True)
+        hx.copy_(X[:, :nl])
+        hr = np.zeros((m, m), order="F")
+        st_, tm_, err_ = api._Stats(), api._Timing(), api._Err()
+        dX = torch.empty((m, ld), dtype=torch.float64, device="cuda") if world > 1 else None
+
+        def e2e_step():
+            if world == 1:
+                rc = api._lib.bgs_factor(ctx.handle, v, n, m, s, 1, hx.data_ptr(), nl,
+                                         hq.data_ptr(), nl, hr.ctypes.data, m,
+                                         ctypes.byref(st_), ctypes.byref(tm_), ctypes.byref(err_))
+                api._raise(rc, err_)
+            else:
+                dX[:, :nl].copy_(hx, non_blocking=True)
+                torch.cuda.synchronize()
+                bgs.factor_device(ctx, v, n, m, s, row0, nl, dX.data_ptr(), ld, Q.data_ptr(), ld)
+                hq.copy_(Q[:, :nl])
+                torch.cuda.synchronize()
+
+        e2e_step()
+        barrier()
+        ts = []
+        for _ in range(max(1, a.steps)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        t_e2e = allmax(sum(ts) / len(ts))
+        e2e = {"value": flops / t_e2e / 1e9, "unit": "GFLOP/s",
+               "ms_per_step": t_e2e * 1e3,
+               "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": n * m * 8 + m * m * 8 * world,
+               "api": "bgs_factor (host X -> host Q, R; the run_factor drop-in)" if world == 1
+               else "per rank: pinned H2D of the shard + bgs_factor_device + D2H of Q"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        try:
+            kind, cores, run = cpu_reference_runner(v, n, m, s, a.seed)
+            rows, _ = pick_sample_rows(run, n, m, a.cpu_seconds)
+            t = run(rows)
+            gf = bgs.variant_flops(v, rows, m, s) / t / 1e9
+            cpu = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": kind,
+                   "sample": f"{a.variant} n={rows} m={m} s={s} N(0,1) (row subsample; cost and "
+                             f"flops both linear in n), {t:.1f} s, run_variant under run_spmd "
+                             f"with P={cores} threads",
+                   "extrapolated_ms_full_n": t * 1e3 * n / rows}
+        except Exception as e:  # the checker must never sink the bench line
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+
+    clocks = cs.summary()
+    if rank == 0:
+        line = {
+            "metric": metric_name(a), "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded i.i.d. N(0,1) generated on device (Philox)",
+            "config": workload_config(a, world),
+            "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"],
+                       "reasons": clocks["reasons"], "samples": clocks["samples"]},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+            "time_ms": ms, "gflops": value,
+            "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": step_bytes / ms / 1e6,
+                              "frac": step_bytes / ms / 1e6 / peak},
+            "kernels": kern, "verify": verify, "wall_s_timed": t_wall,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference_arm(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

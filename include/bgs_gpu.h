@@ -136,6 +136,21 @@ int bgs_metrics_device(bgs_ctx* ctx, long n, long m, long n_local, const double*
                        long ldx, const double* d_q, long ldq, const double* h_r, long ldr,
                        double* loo, double* resid, bgs_error* err);
 
+/* ---- live per-kernel profile (CUDA events on the factorization stream) -------------
+ * When enabled, every kernel class launched by the factorization is bracketed by CUDA
+ * events; bgs_profile_read returns, per class, launches, summed device time and the
+ * ALGORITHMIC bytes / flops those launches had to move / do.
+ * Reading resets the accumulators. */
+typedef struct {
+  char name[32];
+  long launches;
+  double ms;
+  double alg_bytes;
+  double alg_flops;
+} bgs_kernel_stat;
+int bgs_profile_enable(bgs_ctx* ctx, int on);
+int bgs_profile_read(bgs_ctx* ctx, bgs_kernel_stat* out, int cap, int* count);
+
 /* ---- building blocks exposed for parity tests ------------------------------------ */
 /* Tall-skinny Gram A^T B (dense_kernels.hpp:15-24) through the K1 TMA/DMMA kernel:
  * host in/out, out is ma x mb (ld = ma). */

@@ -110,6 +110,16 @@ class _Err(ctypes.Structure):
     ]
 
 
+class _KStat(ctypes.Structure):
+    _fields_ = [
+        ("name", ctypes.c_char * 32),
+        ("launches", ctypes.c_long),
+        ("ms", ctypes.c_double),
+        ("alg_bytes", ctypes.c_double),
+        ("alg_flops", ctypes.c_double),
+    ]
+
+
 class _Timing(ctypes.Structure):
     _fields_ = [
         ("factor_ms", ctypes.c_double),
@@ -143,6 +153,8 @@ def _load() -> ctypes.CDLL:
         "bgs_metrics": ([P, L, L, P, L, P, L, P, L, P, P, P], I),
         "bgs_metrics_device": ([P, L, L, L, P, L, P, L, P, L, P, P, P], I),
         "bgs_gram": ([P, P, L, L, P, L, P, P], I),
+        "bgs_profile_enable": ([P, I], I),
+        "bgs_profile_read": ([P, P, I, P], I),
         "bgs_tsqr": ([P, P, L, L, P, P, P], I),
     }
     for name, (args, res) in sig.items():
@@ -159,6 +171,7 @@ EXPORTED_SYMBOLS = (
     "bgs_shard_rows", "bgs_ctx_create", "bgs_ctx_destroy", "bgs_nccl_unique_id",
     "bgs_device_info", "bgs_factor", "bgs_factor_device", "bgs_gen_gaussian_device",
     "bgs_gen_gaussian_host", "bgs_metrics", "bgs_metrics_device", "bgs_gram", "bgs_tsqr",
+    "bgs_profile_enable", "bgs_profile_read",
 )
 
 
@@ -293,6 +306,19 @@ class Context:
     @property
     def handle(self) -> ctypes.c_void_p:
         return self._h
+
+    def profile(self, on: bool = True) -> None:
+        """Bracket every kernel class of the factorization with CUDA events."""
+        _lib.bgs_profile_enable(self._h, 1 if on else 0)
+
+    def read_profile(self) -> Dict[str, Dict[str, float]]:
+        """Per kernel class: launches, device ms, algorithmic bytes / flops (resets)."""
+        arr = (_KStat * 64)()
+        cnt = ctypes.c_int()
+        _lib.bgs_profile_read(self._h, arr, 64, ctypes.byref(cnt))
+        return {arr[i].name.decode(): dict(launches=int(arr[i].launches), ms=arr[i].ms,
+                                           alg_bytes=arr[i].alg_bytes, alg_flops=arr[i].alg_flops)
+                for i in range(min(cnt.value, 64))}
 
     def close(self) -> None:
         if self._h:

@@ -199,6 +199,46 @@ struct bgs_ctx {
   DBuf tsqr_ws, tsqr_bounds, tsqr_trees, roots, roots_all, cross_ws, cross_m, metrics;
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
   int launches = 0;
+  // live profiler: event pairs per launch, resolved after the stream syncs
+  struct ProfClass {
+    std::string name;
+    long launches = 0;
+    double ms = 0, bytes = 0, flops = 0;
+  };
+  struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  bool prof_on = false;
+  std::vector<ProfClass> prof;
+  std::vector<ProfRec> pending;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreate(&e));
+    return e;
+  }
+  int prof_class(const char* name) {
+    for (size_t i = 0; i < prof.size(); ++i)
+      if (prof[i].name == name) return (int)i;
+    prof.push_back(ProfClass{name});
+    return (int)prof.size() - 1;
+  }
+  // Resolve recorded pairs (the stream must have completed them).
+  void prof_resolve() {
+    for (auto& p : pending) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) prof[p.cls].ms += ms;
+      event_pool.push_back(p.a);
+      event_pool.push_back(p.b);
+    }
+    pending.clear();
+  }
   ~bgs_ctx() {
     for (DBuf* b : {&partial, &G, &scolA, &scolB, &sdiag, &ydiag, &save, &r1, &r2, &rtop, &R,
                     &status, &tsqr_ws, &tsqr_bounds, &tsqr_trees, &roots, &roots_all, &cross_ws,
@@ -206,6 +246,11 @@ struct bgs_ctx {
       b->release();
     for (auto& b : sx) b.release();
     for (auto& b : sq) b.release();
+    for (auto& p : pending) {
+      event_pool.push_back(p.a);
+      event_pool.push_back(p.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -260,6 +305,28 @@ class Runner {
 
   Runner(bgs_ctx* ctx, int v, long n_, long m_, long s_, int P_, bool nccl_, bgs_stats* st)
       : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {}
+
+  // RAII bracket of one launch (or launch group) of a kernel class for the profiler.
+  struct Prof {
+    bgs_ctx* c;
+    int cls = -1;
+    cudaEvent_t a = nullptr;
+    Prof(bgs_ctx* ctx, const char* name, double bytes, double flops) : c(ctx) {
+      if (!c->prof_on) return;
+      cls = c->prof_class(name);
+      c->prof[cls].launches += 1;
+      c->prof[cls].bytes += bytes;
+      c->prof[cls].flops += flops;
+      a = c->get_event();
+      CUDA_OK(cudaEventRecord(a, c->stream));
+    }
+    ~Prof() {
+      if (cls < 0) return;
+      cudaEvent_t b = c->get_event();
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({cls, a, b});
+    }
+  };
 
   void record(const char* label, long w) {
     if (!stats) return;
@@ -382,6 +449,8 @@ class Runner {
         if (sp.nspans == 2) p.map[1] = sp.sp[1].src == SX ? x.mapX : x.mapQ;
         p.n_rows = x.rows;
         p.partial = c->partial.d() + per_cta * cta_base;
+        Prof pr(c, "gram", 8.0 * x.rows * (sp.sp[0].ncols + (sp.nspans == 2 ? sp.sp[1].ncols : 0)),
+                2.0 * x.rows * (double)(lc[0] + (span1_left ? lc[1] : 0)) * sp.N);
         CUDA_OK(gram_partials_launch(p, grid, c->stream, &c->launches));
       } else {
         CUDA_OK(cudaMemsetAsync(c->partial.d() + per_cta * cta_base, 0,
@@ -390,10 +459,15 @@ class Runner {
       cta_base += grid;
     }
     p.partial = c->partial.d();
-    CUDA_OK(gram_reduce_launch(p, cta_base, c->G.d(), c->stream, &c->launches));
-    if (use_nccl && do_allreduce)
+    {
+      Prof pr(c, "gram_reduce", (double)cta_base * per_cta * 8.0, 0.0);
+      CUDA_OK(gram_reduce_launch(p, cta_base, c->G.d(), c->stream, &c->launches));
+    }
+    if (use_nccl && do_allreduce) {
+      Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
       NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
                                c->stream));
+    }
     if (count_sync) record(label, (long)M * p.N);
     return M;
   }
@@ -435,6 +509,9 @@ class Runner {
         p.CB = u.CB; p.ldcb = u.ldcb; p.TB = u.TB; p.ldtb = s;
       }
       p.status = status;
+      const int nout = (u.has_a ? 1 : 0) + (u.has_b ? 1 : 0);
+      Prof pr(c, "update", 8.0 * x.rows * ((double)u.kp + 2.0 * s * nout),
+              2.0 * x.rows * (double)u.kp * s * nout + (double)x.rows * s * s * nout);
       CUDA_OK(update_launch(p, c->sms, c->stream, &c->launches));
     }
   }
@@ -445,6 +522,7 @@ class Runner {
     p.R = c->R.d();
     p.ldr = (int)m;
     p.status = status;
+    Prof pr(c, "small", 0.0, 0.0);
     CUDA_OK(small_launch(p, c->stream, &c->launches));
   }
 
@@ -458,13 +536,17 @@ class Runner {
     const long* bounds = static_cast<const long*>(c->tsqr_bounds.p);
     const int* trees = static_cast<const int*>(c->tsqr_trees.p);
     for (auto& x : sh) {
+      Prof pr(c, "tsqr_leaf", 16.0 * x.rows * s, 8.0 * x.rows * s * s);
       CUDA_OK(tsqr_leaf_launch(colp(x, src, scol_), src == SX ? x.ldx : x.ldq, qcol(x, dcol),
                                x.ldq, bounds + x.bound_base, x.n_leaves, x.hmax, (int)s,
                                tsqr_ws_R(ws) + (size_t)x.leaf_base * ss, status, c->stream,
                                &c->launches));
     }
-    CUDA_OK(tsqr_up_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, c->roots.d(), status,
-                           c->stream, &c->launches));
+    {
+      Prof pr(c, "tsqr_tree", 0.0, 0.0);
+      CUDA_OK(tsqr_up_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, c->roots.d(), status,
+                             c->stream, &c->launches));
+    }
     const double* all_roots = c->roots.d();
     if (use_nccl) {
       NCCL_OK(nccl().GroupStart());
@@ -475,12 +557,16 @@ class Runner {
       NCCL_OK(nccl().GroupEnd());
       all_roots = c->roots_all.d();
     }
-    CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout, c->cross_m.d(),
-                              status, c->stream, &c->launches));
-    const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
-    CUDA_OK(tsqr_down_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, mtop, status, c->stream,
-                             &c->launches));
+    {
+      Prof pr(c, "tsqr_tree", 0.0, 0.0);
+      CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout,
+                                c->cross_m.d(), status, c->stream, &c->launches));
+      const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
+      CUDA_OK(tsqr_down_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, mtop, status, c->stream,
+                               &c->launches));
+    }
     for (auto& x : sh) {
+      Prof pr(c, "tsqr_apply", 16.0 * x.rows * s, 2.0 * x.rows * s * s);
       CUDA_OK(tsqr_apply_launch(qcol(x, dcol), x.ldq, bounds + x.bound_base, x.n_leaves, (int)s,
                                 tsqr_ws_M(ws, tsqr_L, (int)s) + (size_t)x.leaf_base * ss, status,
                                 c->stream, &c->launches));
@@ -964,6 +1050,7 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
     CUDA_OK(cudaEventRecord(c->e1, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaGetLastError());
+    c->prof_resolve();
     run.check_status();
     for (int rk = 0; rk < procs; ++rk) {
       const Shard& sh = run.sh[rk];
@@ -1022,6 +1109,7 @@ int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0
     CUDA_OK(cudaEventRecord(c->e1, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaGetLastError());
+    c->prof_resolve();
     run.check_status();
     if (h_r)
       CUDA_OK(cudaMemcpy2D(h_r, ldr * sizeof(double), c->R.p, m * sizeof(double), m * sizeof(double),
@@ -1197,6 +1285,34 @@ int bgs_metrics(bgs_ctx* c, long n, long m, const double* x, long ldx, const dou
     put_err(err, f);
     return f.code;
   }
+}
+
+int bgs_profile_enable(bgs_ctx* c, int on) {
+  if (!c) return BGS_E_CUDA;
+  c->prof_on = on != 0;
+  return BGS_OK;
+}
+
+int bgs_profile_read(bgs_ctx* c, bgs_kernel_stat* out, int cap, int* count) {
+  if (!c) return BGS_E_CUDA;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->prof_resolve();
+  int n = 0;
+  for (auto& p : c->prof) {
+    if (n < cap && out) {
+      memset(&out[n], 0, sizeof out[n]);
+      snprintf(out[n].name, sizeof out[n].name, "%s", p.name.c_str());
+      out[n].launches = p.launches;
+      out[n].ms = p.ms;
+      out[n].alg_bytes = p.bytes;
+      out[n].alg_flops = p.flops;
+    }
+    ++n;
+  }
+  if (count) *count = n;
+  c->prof.clear();
+  return BGS_OK;
 }
 
 int bgs_gram(bgs_ctx* c, const double* a, long n, long ma, const double* b, long mb, double* out,
