@@ -109,7 +109,8 @@ int bgs_factor(bgs_ctx* ctx, int variant, long n, long m, long s, int procs,
 /* ---- device-resident per-rank entry (run_variant on a DistBlockMatrix,
  * bcgs.hpp:49-50).  This rank owns rows [row0, row0 + n_local) of the global n x m
  * matrix (the ceil split of dist_block.cpp:37-43).  d_x / d_q are device pointers
- * (n_local x m, leading dimensions ldx / ldq, both even).  R is replicated: written to
+ * (n_local x m, leading dimensions ldx / ldq >= n_local rounded up to 16, 16-byte aligned
+ * columns: the TMA tile engine reads whole 16-row blocks; rows past n_local are ignored).  R is replicated: written to
  * host memory h_r (m x m, ldr) identically on every rank.  Collectives use the ctx's
  * NCCL communicator (nranks > 1). */
 int bgs_factor_device(bgs_ctx* ctx, int variant, long n, long m, long s, long row0,

@@ -8,6 +8,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #define BGS_DEV __device__ __forceinline__
 
@@ -84,6 +85,31 @@ BGS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Single probe of an mbarrier phase (true when the phase with `parity` has completed).
+BGS_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Debug wait: traps with a diagnostic instead of hanging (BGS_TILE_DBG & 64).
+BGS_DEV void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int tag, int it) {
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > (1ll << 32)) {
+      printf("[bgs hang] block %d thread %d tag %d iteration %d parity %u\n", blockIdx.x,
+             threadIdx.x, tag, it, parity);
+      __trap();
+    }
+  }
+}
+
 // 2-D tiled TMA load global -> shared, completion on an mbarrier (SASS: UTMALDG).
 BGS_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
                          int c1) {
@@ -91,6 +117,16 @@ BGS_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, 
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 3-D tiled TMA load (the {16 rows, row-block, column} view of a column-major matrix).
+BGS_DEV void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                         int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 

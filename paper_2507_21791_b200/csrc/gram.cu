@@ -1,40 +1,105 @@
-// gram.cu — K1: tall-skinny Gram  G = L^T R  on fp64 tensor cores (DMMA), TMA-fed.
+// gram.cu — the tile engine: K1 (tall-skinny Gram on fp64 tensor cores) and K12 (the
+// block update of step k fused in front of the Gram of step k+1).
 //
-// Replaces fused_gram (dist_block.cpp:79-88) + gram_accumulate (dense_kernels.cpp:10-27)
-// + the per-rank half of exact_allreduce (communicator.cpp:226-250).  The reference
-// accumulates every product exactly in a 2176-bit fixed-point register; here each
-// 16-row stage is contracted with DMMA.8x8x4 and the stage sums are folded into a
-// double-double (hi, lo) accumulator every FLUSH stages, then CTA partials are summed
-// in a fixed order in double-double (gram_reduce) — deterministic, and accurate to
-// O(16u) per entry instead of O(n u).
+// K1 replaces fused_gram (dist_block.cpp:79-88) + gram_accumulate (dense_kernels.cpp:10-27)
+// + the per-rank half of exact_allreduce (communicator.cpp:226-250).  K12 additionally
+// replaces the local_axpy_block / scale_right_block / set_block sequence that sits between
+// two syncs of onesync_impl (bcgs.cpp:329-331, 346-359) and pipi_impl (bcgs.cpp:196-214):
 //
-// Data layout: the operand columns come from up to two column spans of column-major
-// matrices (the Q buffer and X), each addressed by a CUtensorMap.  One pipeline stage =
-// 16 rows x (all boxes); a box = 16 rows x 8 columns = 1 KB, SWIZZLE_128B, so a stage of
-// a (k+2)s = 408-column operand is 51 KB and the whole operand row-tile streams from HBM
-// exactly once.  The right operand R is a set of columns that are already in the tile
-// (BlockSpan semantics of the reference: R's columns are a suffix of L's, or of the
-// second span), so it costs no extra HBM traffic.
+//   A = (srcA - Qp CA) TA^{-1}            e.g. Q_k     = (U_k - Q_{1:k} Y) Y_kk^{-1}
+//   B = (srcB - Qp CB - A S2) TB^{-1}     e.g. U_{k+1} = (X_{k+1} - Q_{1:k} Z - Q_k S2) S^{-1}
+//   G = [tile]^T [right columns]          the next step's fused Gram, on the updated tile
 //
-// Roles: warp 0 lane 0 = TMA producer; warps 1..W = DMMA consumers.  Consumer warp w owns
-// m-tiles (boxes) w, w+W, ... and all n-tiles; per k-step (4 rows) one DMMA per
-// (m-tile, n-tile).  Fragment loads are conflict-free LDS.128 thanks to the swizzle.
+// so each block step streams the Q prefix from HBM once instead of twice.
+//
+// Accuracy: the reference accumulates every product exactly (2176-bit fixed point).  Here
+// each RS-row stage is contracted with DMMA.8x8x4 into a fresh accumulator that is folded
+// into a double-double (hi, lo) pair every GRAM_FLUSH stages; CTA partials are summed in a
+// fixed order in double-double (gram_reduce) — deterministic, O(RS u) per entry.
+//
+// Tile geometry.  A stage is RS = 16H rows (H = 2 or 4) x all tile columns, loaded by TMA
+// through a 3-D view of the column-major matrix: dims {16, ceil(rows/16), cols}, strides
+// {128 B, ld*8 B}, box {16, H, w}, SWIZZLE_128B.  Each column's RS rows are one contiguous
+// 16H*8-byte run (>= 256 B: what keeps HBM near 6.9 TB/s; 128-byte pieces cap it at
+// ~4.6 TB/s) and each box moves w in {128, 64, 32, 16, 8} columns (TMA costs ~450 cycles per
+// box per SM, so spans are cut greedily into the widest boxes; profiles/r01_tma_*.log).
+// In shared memory, 128-byte line L = H*c + h holds rows 16h..16h+15 of tile column c, its
+// 16-byte chunk j stored at chunk j ^ (L & 7).  Both fragment shapes are conflict-free:
+//   Gram (column-major, lane = (col ii, k kk)): two LDS.128 per 4 rows; odd-ii lanes fetch
+//     the two chunks in swapped order (then swap back) so a quarter-warp hits 8 chunks;
+//   update (row-major, lane = (row ii, col kk)): one LDS.64; with H = 2 the four columns of
+//     a k-step sit on lines with distinct (L & 7), so 16 lanes hit 16 distinct slots.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace bgs {
 
-template <int NT, int W, int MTW, bool COMP>
-__global__ void __launch_bounds__(32 * (W + 1), 1)
-    gram_kernel(const __grid_constant__ GramParams p) {
+namespace {
+
+// 8 warps = 2 per scheduler (the 64K register file allows 255 registers per thread).
+// Warp 7 lane 0 issues the TMA.  K1: warps 0-6 run the Gram, warp 7 only streams.
+// K12: warps 0-6 split the update k-steps while warp 7 refills the freed slot (a TMA box
+// keeps the issuing thread ~1 cycle per 128-byte line), then all 8 warps run the
+// epilogue and the Gram.
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = 32 * kConsumerWarps;
+constexpr int kUpdWarps = 7;
+constexpr int kProducerWarp = 7;
+template <bool UPD>
+struct Roles {
+  static constexpr int WG = UPD ? 8 : 7;  // Gram warps
+};
+
+// byte offset of the 8-byte element (row r, tile column c) inside a stage
+template <int H>
+BGS_DEV uint32_t elem_off(int col, int r) {
+  const int line = H * col + (r >> 4);
+  const int chunk = ((r & 15) >> 1) ^ (line & 7);
+  return (uint32_t)(line * 128 + chunk * 16 + (r & 1) * 8);
+}
+
+// Gram fragment: rows 16h + 4kk + {0,1,2,3} of tile column `col`.
+template <int H>
+BGS_DEV void frag4(uint32_t stage, int col, int h, int kk, int odd, double (&v)[4]) {
+  const int line = H * col + h;
+  const uint32_t b = stage + (uint32_t)(line * 128);
+  const int c0 = (2 * kk + odd) ^ (line & 7), c1 = (2 * kk + 1 - odd) ^ (line & 7);
+  const double2 x0 = lds128(b + (uint32_t)(c0 << 4));
+  const double2 x1 = lds128(b + (uint32_t)(c1 << 4));
+  v[0] = odd ? x1.x : x0.x;
+  v[1] = odd ? x1.y : x0.y;
+  v[2] = odd ? x0.x : x1.x;
+  v[3] = odd ? x0.y : x1.y;
+}
+
+// Named barrier over the warps that run the stage loop (all 8 in K12, 0-6 in K1).
+template <int NWARPS>
+BGS_DEV void bar_warps() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NWARPS) : "memory");
+}
+
+constexpr int SMAX_E = 8;  // fused epilogue supports s <= 8 (K12 is instantiated for s <= 4)
+
+}  // namespace
+
+template <int H, int NT, int MTW, bool COMP, bool UPD, int KW>
+__global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant__ TileParams p) {
   if (p.status && status_bad(p.status)) return;
+  constexpr int RS = 16 * H;
+  constexpr int W = kConsumerWarps;   // epilogue / barrier width
+  constexpr int WG = Roles<UPD>::WG;  // Gram m-tile stride
+  constexpr int WU = kUpdWarps;       // update k-step stride
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
-  const int stage_bytes = p.nboxes * 1024;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  const int stage_bytes = p.units * 8 * RS * 8;
+  double* red = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);  // [W][8][RS+4]
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      reinterpret_cast<unsigned char*>(red) + (UPD ? (size_t)W * 8 * (RS + 4) * sizeof(double) : 0));
   uint64_t* empty = full + S;
+  __shared__ double ep_ta[SMAX_E * SMAX_E], ep_tb[SMAX_E * SMAX_E], ep_s2[SMAX_E * SMAX_E];
+  __shared__ double ep_tai[SMAX_E * SMAX_E], ep_tbi[SMAX_E * SMAX_E], ep_w[SMAX_E * SMAX_E];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long T = p.total_stages;
@@ -45,58 +110,105 @@ __global__ void __launch_bounds__(32 * (W + 1), 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], W);
+      mbar_init(&empty[i], WG);  // every warp that consumes the slot releases it
     }
     fence_mbar_init();
   }
+  if (UPD) {
+    // Epilogue factors, once per CTA: TA^{-1}, TB^{-1} (upper, by back-substitution on the
+    // identity, column j by thread j) and W = S2 TB^{-1}; the per-row epilogue then needs
+    // only short dot products instead of a serial substitution per row.
+    const int s = p.s;
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+      const int i = e % s, j = e / s;
+      ep_ta[i + j * SMAX_E] = p.TA ? p.TA[i + j * s] : (i == j ? 1.0 : 0.0);
+      ep_tb[i + j * SMAX_E] = p.TB ? p.TB[i + j * s] : (i == j ? 1.0 : 0.0);
+      ep_s2[i + j * SMAX_E] = (p.upd_a && p.upd_b) ? p.CB[p.kp + i + (size_t)j * p.ldcb] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * s) {
+      const bool isb = threadIdx.x >= s;
+      const int j = isb ? threadIdx.x - s : threadIdx.x;
+      const double* T = isb ? ep_tb : ep_ta;
+      double* Ti = isb ? ep_tbi : ep_tai;
+      for (int i = s - 1; i >= 0; --i) {  // column j of T^{-1}: T y = e_j
+        double acc = (i == j) ? 1.0 : 0.0;
+        for (int l = i + 1; l < s; ++l) acc -= T[i + l * SMAX_E] * Ti[l + j * SMAX_E];
+        Ti[i + j * SMAX_E] = acc / T[i + i * SMAX_E];
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+      const int m = e % s, j = e / s;
+      double acc = 0.0;
+      for (int l = 0; l < s; ++l) acc += ep_s2[m + l * SMAX_E] * ep_tbi[l + j * SMAX_E];
+      ep_w[m + j * SMAX_E] = acc;
+    }
+  }
   __syncthreads();
 
-  if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      prefetch_tmap(&p.map[0]);
-      if (p.nbox[1] > 0) prefetch_tmap(&p.map[1]);
-      for (int it = 0; it < nst; ++it) {
-        const int slot = it % S;
-        const int round = it / S;
-        mbar_wait(&empty[slot], (round & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)stage_bytes);
-        unsigned char* dst = smem + (size_t)slot * stage_bytes;
-        const int row = (int)((st0 + it) * 16);
-        for (int b = 0; b < p.nbox[0]; ++b)
-          tma_load_2d(dst + b * 1024, &p.map[0], &full[slot], row, p.col0[0] + 8 * b);
-        for (int b = 0; b < p.nbox[1]; ++b)
-          tma_load_2d(dst + (p.nbox[0] + b) * 1024, &p.map[1], &full[slot], row,
-                      p.col0[1] + 8 * b);
+  // ---------------- TMA issue (thread 0): greedy widest boxes per span ----------------
+  auto issue_stage = [&](int it) {
+    const int slot = it % S;
+    mbar_arrive_expect_tx(&full[slot], (uint32_t)stage_bytes);
+    unsigned char* dst = smem + (size_t)slot * stage_bytes;
+    const int rb = (int)((st0 + it) * H);  // first 16-row block of this stage
+    int u = 0;                              // 8-column units issued so far (tile column = 8u)
+    for (int sp = 0; sp < 2; ++sp) {
+      int left = p.units_span[sp], c = p.col0[sp];
+      while (left > 0) {
+        int wi;  // width index: 0:128, 1:64, 2:32, 3:16, 4:8 columns
+        const CUtensorMap* mp;
+        if (sp == 0) {
+          wi = left >= 16 ? 0 : left >= 8 ? 1 : left >= 4 ? 2 : left >= 2 ? 3 : 4;
+          mp = &p.map0[wi];
+        } else {
+          wi = left >= 2 ? 3 : 4;
+          mp = &p.map1[wi - 3];
+        }
+        const int wu = 16 >> wi;
+        tma_load_3d(dst + (size_t)u * 8 * RS * 8, mp, &full[slot], 0, rb, c);
+        u += wu;
+        c += 8 * wu;
+        left -= wu;
+      }
+    }
+  };
+  const bool producer = threadIdx.x == 32 * kProducerWarp;
+  if (producer) {
+    for (int i = 0; i < 5; ++i) prefetch_tmap(&p.map0[i]);
+    for (int i = 0; i < 2; ++i) prefetch_tmap(&p.map1[i]);
+    for (int it = 0; it < S && it < nst; ++it) issue_stage(it);
+  }
+  if (!UPD && warp == kProducerWarp) {
+    // K1: dedicated producer warp
+    if (producer) {
+      for (int it = 0; it + S < nst; ++it) {
+        mbar_wait(&empty[it % S], (it / S) & 1);
+        issue_stage(it + S);
       }
     }
     return;
   }
 
-  // ---------------- DMMA consumers ----------------
-  const int cw = warp - 1;
-  const int kk = lane & 3, ii = lane >> 2;
+  // ---------------- consumers ----------------
+  const int cw = warp;
+  const int kk = lane & 3, ii = lane >> 2, odd = ii & 1;
+  (void)lane;
   int cnt = 0;
-  for (int t = cw; t < p.mt_out; t += W) ++cnt;
-
-  uint32_t boff0[NT], boff1[NT];
+  for (int t = cw; t < p.mt_out; t += WG) ++cnt;
+  int bcol[NT];
   bool bval[NT];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int col = p.rcol[nt * 8 + ii];
     bval[nt] = col >= 0;
-    const int c = col >= 0 ? col : 0;
-    boff0[nt] = swz(c, 2 * kk);
-    boff1[nt] = swz(c, 2 * kk + 1);
+    bcol[nt] = col >= 0 ? col : 0;
   }
-  uint32_t aoff0[MTW], aoff1[MTW];
+
+  int acol[MTW];
 #pragma unroll
-  for (int j = 0; j < MTW; ++j) {
-    const int t = cw + W * (j < cnt ? j : 0);
-    const int col = 8 * t + ii;
-    aoff0[j] = swz(col, 2 * kk);
-    aoff1[j] = swz(col, 2 * kk + 1);
-  }
+  for (int j = 0; j < MTW; ++j) acol[j] = 8 * (j < cnt ? cw + WG * j : 0) + ii;
 
   double acc[MTW][NT][2];
   double hi[COMP ? MTW : 1][NT][2];
@@ -109,6 +221,24 @@ __global__ void __launch_bounds__(32 * (W + 1), 1)
       if (COMP) hi[j][nt][0] = hi[j][nt][1] = lo[j][nt][0] = lo[j][nt][1] = 0.0;
     }
 
+  // Update coefficients as DMMA B fragments held in registers for the whole kernel:
+  // this warp owns k-steps g = cw + W*j (columns 4g..4g+3 of the prefix); lane holds
+  // C[4g + kk][n = ii] where C = [CA | CB] (kp x 2s, zero padded).
+  double bco[UPD ? KW : 1];
+  const int s = p.s;
+  if (UPD) {
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const int c = cw < WU ? 4 * (cw + WU * j) + kk : p.kp;  // warp 7: no update k-steps
+      double v = 0.0;
+      if (c < p.kp) {
+        if (ii < s && p.upd_a) v = p.CA[c + (size_t)ii * p.ldca];
+        else if (ii >= s && ii < 2 * s && p.upd_b) v = p.CB[c + (size_t)(ii - s) * p.ldcb];
+      }
+      bco[j] = v;
+    }
+  }
+
   auto flush = [&]() {
     if (COMP) {
 #pragma unroll
@@ -117,9 +247,9 @@ __global__ void __launch_bounds__(32 * (W + 1), 1)
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            double s, err;
-            two_sum(hi[j][nt][e], acc[j][nt][e], s, err);
-            hi[j][nt][e] = s;
+            double sm, err;
+            two_sum(hi[j][nt][e], acc[j][nt][e], sm, err);
+            hi[j][nt][e] = sm;
             lo[j][nt][e] += err;
             acc[j][nt][e] = 0.0;
           }
@@ -128,42 +258,192 @@ __global__ void __launch_bounds__(32 * (W + 1), 1)
 
   const uint32_t sbase = smem_u32(smem);
   int since = 0;
+  const bool prof = p.phase && threadIdx.x == 0;
+  // wait, update, reduce+bar, epilogue+bar, gram, total, fence+arrive, refill issue, flush
+  unsigned long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ph_prod = 0;                   // thread 0 waiting to refill a slot
+  const unsigned long long t_begin = prof ? clock64() : 0;
   for (int it = 0; it < nst; ++it) {
     const int slot = it % S;
-    mbar_wait(&full[slot], (it / S) & 1);
+    unsigned long long t0 = prof ? clock64() : 0;
+    if (p.dbg & 64) mbar_wait_dbg(&full[slot], (it / S) & 1, 1, it);
+    else mbar_wait(&full[slot], (it / S) & 1);
+    unsigned long long t1 = prof ? clock64() : 0;
+    if (prof) ph[0] += t1 - t0;
     const uint32_t base = sbase + (uint32_t)(slot * stage_bytes);
-    double b[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      double2 v0 = lds128(base + boff0[nt]);
-      double2 v1 = lds128(base + boff1[nt]);
-      b[nt][0] = bval[nt] ? v0.x : 0.0;
-      b[nt][1] = bval[nt] ? v0.y : 0.0;
-      b[nt][2] = bval[nt] ? v1.x : 0.0;
-      b[nt][3] = bval[nt] ? v1.y : 0.0;
+    const long row0 = (st0 + it) * RS;
+    const int vrows = (int)((p.n_rows - row0) < RS ? (p.n_rows - row0) : RS);
+    if (vrows < RS) {
+      // rows past the shard end inside the last 16-row block are not TMA zero-filled
+      const int ncol = p.units * 8;
+      for (int e = threadIdx.x; e < ncol * (RS - vrows); e += 32 * W) {
+        const int c = e / (RS - vrows), r = vrows + e % (RS - vrows);
+        sts64(base + elem_off<H>(c, r), 0.0);
+      }
+      bar_warps<WG>();
     }
+
+    if (UPD) {
+      // warp 7 refills the slot released at the end of the previous stage while warps
+      // 0-6 run the update MMAs (stage it-1+S goes into slot (it-1)%S)
+      if (producer && it >= 1 && it - 1 + S < nst) {
+        const unsigned long long tw = p.phase ? clock64() : 0;
+        if (p.dbg & 64) mbar_wait_dbg(&empty[(it - 1) % S], ((it - 1) / S) & 1, 2, it);
+        else mbar_wait(&empty[(it - 1) % S], ((it - 1) / S) & 1);
+        if (p.phase) ph_prod += clock64() - tw;
+        issue_stage(it - 1 + S);
+      }
+      // reconverge warp 7 before anything reaches a bar.sync (an aligned barrier)
+      if (warp == kProducerWarp) __syncwarp();
+      // ---- update MMAs: D[row][n] = sum_c tile[row][c] * C[c][n], k-split over warps ----
+      constexpr int MT_U = RS / 8;
+      // two accumulator sets (even / odd k-steps) -> 2*MT_U independent DMMA chains;
+      // k-steps past kp are predicated to zero instead of branched around.
+      double d[2][MT_U][2];
 #pragma unroll
-    for (int j = 0; j < MTW; ++j) {
-      if (j < cnt) {
-        double2 a0 = lds128(base + aoff0[j]);
-        double2 a1 = lds128(base + aoff1[j]);
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          dmma(acc[j][nt][0], acc[j][nt][1], a0.x, b[nt][0]);
-          dmma(acc[j][nt][0], acc[j][nt][1], a0.y, b[nt][1]);
-          dmma(acc[j][nt][0], acc[j][nt][1], a1.x, b[nt][2]);
-          dmma(acc[j][nt][0], acc[j][nt][1], a1.y, b[nt][3]);
+        for (int mt = 0; mt < MT_U; ++mt) d[e][mt][0] = d[e][mt][1] = 0.0;
+      if (!(p.dbg & 4) && cw < WU) {
+#pragma unroll
+        for (int j = 0; j < KW; ++j) {
+          const int c = 4 * (cw + WU * j) + kk;
+          const bool in = c < p.kp && cw < WU;
+          double av[MT_U];
+#pragma unroll
+          for (int mt = 0; mt < MT_U; ++mt) {
+            const double v = lds64(base + elem_off<H>(in ? c : 0, 8 * mt + ii));
+            av[mt] = in ? v : 0.0;
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT_U; ++mt) dmma(d[j & 1][mt][0], d[j & 1][mt][1], av[mt], bco[j]);
         }
       }
+#pragma unroll
+      for (int mt = 0; mt < MT_U; ++mt) {
+        d[0][mt][0] += d[1][mt][0];
+        d[0][mt][1] += d[1][mt][1];
+      }
+      if (prof) { const unsigned long long t = clock64(); ph[1] += t - t1; t1 = t; }
+      // partial sums, transposed with a padded row stride: red[warp][n][RL], RL = RS + 4
+      constexpr int RL = RS + 4;
+      if (cw < WU) {
+#pragma unroll
+        for (int mt = 0; mt < MT_U; ++mt) {
+          double* rr = red + ((size_t)cw * 8 + 2 * kk) * RL + 8 * mt + ii;
+          rr[0] = d[0][mt][0];
+          rr[RL] = d[0][mt][1];
+        }
+      }
+      bar_warps<WG>();
+      if (prof) { const unsigned long long t = clock64(); ph[2] += t - t1; t1 = t; }
+      // ---- epilogue: a quad of lanes per row (lane j of the quad owns column j) ----
+      // Sum the W warp partials in order, then back-substitute across the quad with
+      // shuffles: A = (srcA - Qp CA) TA^{-1}, B = (srcB - Qp CB - A S2) TB^{-1}.
+      const uint32_t red_s = smem_u32(red);
+      for (int e0 = 0; e0 < 4 * RS && !(p.dbg & 16); e0 += 32 * W) {
+        const int e = e0 + (int)threadIdx.x;
+        if (e >= 4 * RS) break;  // whole warps (4 RS and 32 W are multiples of 32)
+        const int r = e >> 2, j = e & 3;
+        const bool jv = j < s;
+        const int quad = (int)(threadIdx.x & 31) & ~3;
+        // warp partials, two independent halves per sum
+        double pa[2] = {0.0, 0.0}, pb[2] = {0.0, 0.0};
+#pragma unroll
+        for (int w = 0; w < WU; ++w) {
+          pa[w & 1] += lds64(red_s + (uint32_t)((((size_t)w * 8 + j) * RL + r) * 8));
+          pb[w & 1] += lds64(red_s + (uint32_t)((((size_t)w * 8 + (jv ? s + j : j)) * RL + r) * 8));
+        }
+        const double aA = pa[0] + pa[1], aB = pb[0] + pb[1];
+        const bool live = r < vrows;
+        const long grow = row0 + r;
+        const uint32_t offA = base + elem_off<H>(p.colA + (jv ? j : 0), r);
+        const uint32_t offB = base + elem_off<H>(p.colB + (jv ? j : 0), r);
+        const double uA = p.upd_a ? lds64(offA) : 0.0;
+        const double uB = p.upd_b ? lds64(offB) : 0.0;
+        // A_j = sum_{l<=j} (srcA - acc)_l TA^{-1}[l][j]
+        double dA = jv ? uA - aA : 0.0, q[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) q[l] = __shfl_sync(0xffffffffu, dA, quad | l);
+        double x = 0.0;
+        if (p.upd_a) {
+#pragma unroll
+          for (int l = 0; l < 4; ++l)
+            if (l <= j && l < s) x += q[l] * ep_tai[l + j * SMAX_E];
+#pragma unroll
+          for (int l = 0; l < 4; ++l) q[l] = __shfl_sync(0xffffffffu, x, quad | l);
+          if (jv) {
+            sts64(offA, x);
+            if (live && !(p.dbg & 2)) p.dstA[grow + (size_t)j * p.lddA] = x;
+          }
+        } else {
+#pragma unroll
+          for (int l = 0; l < 4; ++l) q[l] = 0.0;
+        }
+        if (p.upd_b) {
+          // B_j = sum_{l<=j} (srcB - acc)_l TB^{-1}[l][j] - sum_m A_m (S2 TB^{-1})[m][j]
+          const double dB = jv ? uB - aB : 0.0;
+          double y = 0.0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            const double dl = __shfl_sync(0xffffffffu, dB, quad | l);
+            if (l <= j && l < s) y += dl * ep_tbi[l + j * SMAX_E];
+            if (l < s && jv) y -= q[l] * ep_w[l + j * SMAX_E];
+          }
+          if (jv) {
+            sts64(offB, y);
+            if (live && !(p.dbg & 2)) p.dstB[grow + (size_t)j * p.lddB] = y;
+          }
+        }
+      }
+      bar_warps<WG>();
+      if (prof) { const unsigned long long t = clock64(); ph[3] += t - t1; t1 = t; }
     }
+
+    // ---- Gram on the (updated) tile ----
+    // Every warp runs MTW m-tiles (the tail warps clamp to a valid tile and drop the
+    // result), loads all A fragments of a 16-row half first, then issues the DMMAs
+    // k-step-major so consecutive DMMAs are independent (MTW*NT chains in flight).
+    if (!(p.dbg & 8)) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        double b[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          frag4<H>(base, bcol[nt], h, kk, odd, b[nt]);
+          if (!bval[nt]) b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = 0.0;
+        }
+        double a[MTW][4];
+#pragma unroll
+        for (int j = 0; j < MTW; ++j) frag4<H>(base, acol[j], h, kk, odd, a[j]);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+          for (int j = 0; j < MTW; ++j)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[j][nt][0], acc[j][nt][1], a[j][q4], b[nt][q4]);
+      }
+    }
+    if (prof) { const unsigned long long t = clock64(); ph[4] += t - t1; t1 = t; }
+    if (UPD && !(p.dbg & 1)) fence_proxy_async();  // generic smem writes before TMA reuses the slot
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
+    if (prof) { const unsigned long long t = clock64(); ph[6] += t - t1; t1 = t; }
+
+    if (prof) { const unsigned long long t = clock64(); ph[7] += t - t1; t1 = t; }
     if (++since == GRAM_FLUSH) {
       flush();
       since = 0;
     }
+    if (prof) ph[8] += clock64() - t1;
   }
   flush();
+  if (prof) {
+    ph[5] = clock64() - t_begin;
+    for (int i = 0; i < 9; ++i) atomicAdd(&p.phase[blockIdx.x * 16 + i], ph[i]);
+    atomicAdd(&p.phase[blockIdx.x * 16 + 9], (unsigned long long)nst);
+    atomicAdd(&p.phase[blockIdx.x * 16 + 10], ph_prod);
+  }
 
   // ---------------- per-CTA partial (hi, lo) ----------------
   const int N8 = 8 * NT;
@@ -171,52 +451,69 @@ __global__ void __launch_bounds__(32 * (W + 1), 1)
 #pragma unroll
   for (int j = 0; j < MTW; ++j) {
     if (j < cnt) {
-      const int t = cw + W * j;
+      const int t = cw + WG * j;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = nt * 8 + 2 * kk + e;
-          double h = COMP ? hi[j][nt][e] : acc[j][nt][e];
-          double l = COMP ? lo[j][nt][e] : 0.0;
-          part[((size_t)t * 8 + ii) * N8 + n] = make_double2(h, l);
+          const double hv = COMP ? hi[j][nt][e] : acc[j][nt][e];
+          const double lv = COMP ? lo[j][nt][e] : 0.0;
+          part[((size_t)t * 8 + ii) * N8 + n] = make_double2(hv, lv);
         }
     }
   }
 }
 
-// Deterministic cross-CTA reduction in double-double, rank-local.  One thread per
-// output entry; CTA partials are summed in CTA order (fixed, so results are
-// reproducible run to run).  Writes the compact M x N column-major Gram.
-__global__ void gram_reduce_kernel(const double2* __restrict__ part, int G, int mt_out, int N8,
-                                   int N, int nbox0, int lcols0, int lcols1, int M,
-                                   double* __restrict__ out, const DevStatus* status) {
+// Deterministic cross-CTA reduction in double-double, rank-local.  A CTA handles 32
+// output entries with 8 slices each: slice l sums CTA partials g = l, l+8, ... in order,
+// then the 8 slice sums are combined in slice order.  Fixed order -> reproducible.
+constexpr int RED_ENTRIES = 32, RED_SLICES = 8;
+__global__ void __launch_bounds__(RED_ENTRIES * RED_SLICES)
+    gram_reduce_kernel(const double2* __restrict__ part, int G, int mt_out, int N8, int N,
+                       int ubox0, int lcols0, int lcols1, int M, double* __restrict__ out,
+                       const DevStatus* status) {
   if (status && status_bad(status)) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double2 red[RED_SLICES][RED_ENTRIES];
+  const int le = threadIdx.x % RED_ENTRIES, sl = threadIdx.x / RED_ENTRIES;
+  const int idx = blockIdx.x * RED_ENTRIES + le;
   const int per_cta = mt_out * 8 * N8;
-  if (idx >= per_cta) return;
+  double s = 0.0, e = 0.0;
+  if (idx < per_cta) {
+    const double2* ptr = part + idx;
+#pragma unroll 4
+    for (int g = sl; g < G; g += RED_SLICES) {
+      const double2 v = ptr[(size_t)g * per_cta];
+      double s2, err;
+      two_sum(s, v.x, s2, err);
+      s = s2;
+      e += err + v.y;
+    }
+  }
+  red[sl][le] = make_double2(s, e);
+  __syncthreads();
+  if (sl != 0 || idx >= per_cta) return;
+  s = 0.0;
+  e = 0.0;
+  for (int l = 0; l < RED_SLICES; ++l) {
+    const double2 v = red[l][le];
+    double s2, err;
+    two_sum(s, v.x, s2, err);
+    s = s2;
+    e += err + v.y;
+  }
   const int n = idx % N8;
   const int i = (idx / N8) % 8;
   const int t = idx / (8 * N8);
   if (n >= N) return;
   int row;
-  if (t < nbox0) {
+  if (t < ubox0) {
     row = 8 * t + i;
     if (row >= lcols0) return;
   } else {
-    const int r = 8 * (t - nbox0) + i;
+    const int r = 8 * (t - ubox0) + i;
     if (r >= lcols1) return;
     row = lcols0 + r;
-  }
-  double s = 0.0, e = 0.0;
-  const double2* ptr = part + idx;
-#pragma unroll 8
-  for (int g = 0; g < G; ++g) {
-    const double2 v = ptr[(size_t)g * per_cta];
-    double s2, err;
-    two_sum(s, v.x, s2, err);
-    s = s2;
-    e += err + v.y;
   }
   out[row + (size_t)n * M] = s + e;
 }
@@ -224,27 +521,6 @@ __global__ void gram_reduce_kernel(const double2* __restrict__ part, int G, int 
 // ------------------------------------------------------------------------------------
 // Host launchers
 // ------------------------------------------------------------------------------------
-template <int NT, int W, int MTW, bool COMP>
-static cudaError_t launch_one(const GramParams& p, int grid, size_t smem, cudaStream_t st) {
-  auto k = gram_kernel<NT, W, MTW, COMP>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k<<<grid, 32 * (W + 1), smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <int NT>
-static cudaError_t dispatch_mtw(const GramParams& p, int mtw, int grid, size_t smem,
-                                cudaStream_t st) {
-  constexpr bool C2 = NT * 2 * 6 <= 96, C4 = NT * 4 * 6 <= 96, C7 = NT * 7 * 6 <= 96,
-                 C13 = NT * 13 * 6 <= 96;
-  if (mtw <= 2) return launch_one<NT, 8, 2, C2>(p, grid, smem, st);
-  if (mtw <= 4) return launch_one<NT, 8, 4, C4>(p, grid, smem, st);
-  if (mtw <= 7) return launch_one<NT, 8, 7, C7>(p, grid, smem, st);
-  if (mtw <= 13) return launch_one<NT, 8, 13, (NT == 1) && C13>(p, grid, smem, st);
-  return cudaErrorInvalidValue;
-}
-
 int gram_n_tiles(int N) {
   int nt = (N + 7) / 8;
   return nt == 3 ? 4 : nt;
@@ -254,34 +530,108 @@ size_t gram_partial_doubles_per_cta(int mt_out, int N) {
   return (size_t)mt_out * 8 * 8 * gram_n_tiles(N) * 2;
 }
 
-cudaError_t gram_partials_launch(GramParams& p, int grid, cudaStream_t st, int* launches) {
-  const int W = 8;
-  if (p.N < 1 || p.N > 32 || p.mt_out < 1 || grid < 1) return cudaErrorInvalidValue;
-  p.nt = gram_n_tiles(p.N);
-  p.total_stages = (p.n_rows + 15) / 16;
-  const int stage_bytes = p.nboxes * 1024;
-  int S = (GRAM_SMEM_BUDGET - 2048) / stage_bytes;
-  if (S > 16) S = 16;
-  if (S < 2) return cudaErrorInvalidValue;
-  p.stages = S;
-  const size_t smem = (size_t)S * stage_bytes + 1024 + 2 * S * sizeof(uint64_t) + 64;
-  const int mtw = (p.mt_out + W - 1) / W;
-  if (launches) *launches += 1;
-  switch (p.nt) {
-    case 1: return dispatch_mtw<1>(p, mtw, grid, smem, st);
-    case 2: return dispatch_mtw<2>(p, mtw, grid, smem, st);
-    default: return dispatch_mtw<4>(p, mtw, grid, smem, st);
+size_t tile_smem_bytes(int H, int stages, int units, bool upd) {
+  const int RS = 16 * H;
+  return (size_t)stages * units * 8 * RS * 8 +
+         (upd ? (size_t)kConsumerWarps * (RS + 4) * 8 * 8 : 0) + 2 * stages * sizeof(uint64_t) +
+         1024 + 64;
+}
+
+template <int H, int NT, int MTW, bool COMP, bool UPD, int KW>
+static cudaError_t launch_t(const TileParams& p, int grid, cudaStream_t st) {
+  auto k = tile_kernel<H, NT, MTW, COMP, UPD, KW>;
+  const size_t smem = tile_smem_bytes(H, p.stages, p.units, UPD);
+  cudaError_t e = ensure_smem(k, smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+// The tile loops run exactly MTW m-tiles and KW k-steps per warp (predicated, no
+// branches), so instantiations are dense where the block steps live.
+template <int H, int NT>
+static cudaError_t dispatch_gram(const TileParams& p, int mtw, int grid, cudaStream_t st) {
+  constexpr bool CO = NT <= 2;  // double-double folding when the registers allow it
+  switch (mtw) {
+    case 1: return launch_t<H, NT, 1, true, false, 1>(p, grid, st);
+    case 2: return launch_t<H, NT, 2, true, false, 1>(p, grid, st);
+    case 3: return launch_t<H, NT, 3, true, false, 1>(p, grid, st);
+    case 4: return launch_t<H, NT, 4, CO, false, 1>(p, grid, st);
+    case 5: return launch_t<H, NT, 5, CO, false, 1>(p, grid, st);
+    case 6: return launch_t<H, NT, 6, NT == 1, false, 1>(p, grid, st);
+    case 7: return launch_t<H, NT, 7, NT == 1, false, 1>(p, grid, st);
+    case 8: return launch_t<H, NT, 8, NT == 1, false, 1>(p, grid, st);
+    default: break;
+  }
+  if (mtw <= 15) return launch_t<H, NT, 15, false, false, 1>(p, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+template <int H, int MTW>
+static cudaError_t fused_kw(const TileParams& p, int kw, int grid, cudaStream_t st) {
+  constexpr int K1 = 2 * MTW - 1 > 0 ? 2 * MTW - 1 : 1, K2 = 2 * MTW;
+  if (kw <= K1) return launch_t<H, 1, MTW, true, true, K1>(p, grid, st);
+  if (kw <= K2) return launch_t<H, 1, MTW, true, true, K2>(p, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+template <int H>
+static cudaError_t dispatch_fused(const TileParams& p, int mtw, int kw, int grid, cudaStream_t st) {
+  // k-steps per warp track m-tiles per warp (kw ~ 2 mtw along a sweep); widen the
+  // Gram side when the update side needs more.
+  if (kw > 2 * mtw) mtw = (kw + 1) / 2;
+  switch (mtw) {
+    case 1: return fused_kw<H, 1>(p, kw, grid, st);
+    case 2: return fused_kw<H, 2>(p, kw, grid, st);
+    case 3: return fused_kw<H, 3>(p, kw, grid, st);
+    case 4: return fused_kw<H, 4>(p, kw, grid, st);
+    case 5: return fused_kw<H, 5>(p, kw, grid, st);
+    case 6: return fused_kw<H, 6>(p, kw, grid, st);
+    case 7: return fused_kw<H, 7>(p, kw, grid, st);
+    case 8: return fused_kw<H, 8>(p, kw, grid, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t gram_reduce_launch(const GramParams& p, int ctas, double* out, cudaStream_t st,
+bool tile_fused_supported(int s, int kp, int mt_out) {
+  const int kw = ((kp + 3) / 4 + kUpdWarps - 1) / kUpdWarps;
+  int mtw = (mt_out + Roles<true>::WG - 1) / Roles<true>::WG;
+  if (kw > 2 * mtw) mtw = (kw + 1) / 2;
+  return s >= 1 && s <= 4 && kw <= 2 * mtw && mtw <= 8;
+}
+
+cudaError_t tile_launch(TileParams& p, bool upd, int grid, cudaStream_t st, int* launches) {
+  if (p.N < 1 || p.N > 32 || p.mt_out < 1 || grid < 1) return cudaErrorInvalidValue;
+  if (p.H != 2 && p.H != 4) return cudaErrorInvalidValue;
+  p.nt = gram_n_tiles(p.N);
+  p.total_stages = (p.n_rows + 16 * p.H - 1) / (16 * p.H);
+  const int WGv = upd ? Roles<true>::WG : Roles<false>::WG;
+  const int mtw = (p.mt_out + WGv - 1) / WGv;
+  if (launches) *launches += 1;
+  if (upd) {
+    if (p.nt != 1 || p.s > 4) return cudaErrorInvalidValue;
+    const int kw = ((p.kp + 3) / 4 + kUpdWarps - 1) / kUpdWarps;
+    return p.H == 2 ? dispatch_fused<2>(p, mtw, kw, grid, st)
+                    : dispatch_fused<4>(p, mtw, kw, grid, st);
+  }
+  switch (p.nt) {
+    case 1:
+      return p.H == 2 ? dispatch_gram<2, 1>(p, mtw, grid, st) : dispatch_gram<4, 1>(p, mtw, grid, st);
+    case 2:
+      return p.H == 2 ? dispatch_gram<2, 2>(p, mtw, grid, st) : dispatch_gram<4, 2>(p, mtw, grid, st);
+    default:
+      return p.H == 2 ? dispatch_gram<2, 4>(p, mtw, grid, st) : dispatch_gram<4, 4>(p, mtw, grid, st);
+  }
+}
+
+cudaError_t gram_reduce_launch(const TileParams& p, int ctas, double* out, cudaStream_t st,
                                int* launches) {
   const int N8 = 8 * gram_n_tiles(p.N);
   const int entries = p.mt_out * 8 * N8;
-  const int lc1 = p.mt_out > p.nbox[0] ? p.lcols[1] : 0;
-  gram_reduce_kernel<<<(entries + 255) / 256, 256, 0, st>>>(
-      reinterpret_cast<const double2*>(p.partial), ctas, p.mt_out, N8, p.N, p.nbox[0],
-      p.lcols[0], lc1, p.lcols[0] + lc1, out, p.status);
+  const int lc1 = p.mt_out > p.units_span[0] ? p.lcols[1] : 0;
+  gram_reduce_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, RED_ENTRIES * RED_SLICES, 0,
+                       st>>>(reinterpret_cast<const double2*>(p.partial), ctas, p.mt_out, N8, p.N,
+                             p.units_span[0], p.lcols[0], lc1, p.lcols[0] + lc1, out, p.status);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

@@ -7,35 +7,56 @@
 
 namespace bgs {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size class (it
+// is a host-synchronous driver call; doing it per launch starves the GPU).
+cudaError_t ensure_smem_impl(const void* kernel, size_t bytes);
+template <typename K>
+inline cudaError_t ensure_smem(K kernel, size_t bytes) {
+  return ensure_smem_impl(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 struct DevStatus;
 
-// ---------------- K1: Gram (gram.cu) ----------------
-constexpr int GRAM_FLUSH = 4;               // stages (x16 rows) between double-double folds
-constexpr int GRAM_SMEM_BUDGET = 210 * 1024;  // bytes of stage ring per CTA
+// ---------------- K1 / K12: the tile engine (gram.cu) ----------------
+constexpr int GRAM_FLUSH = 2;                  // stages between double-double folds
+// Dynamic shared memory budget per CTA: 227 KB minus the kernel's static shared memory
+// and the per-block reservation (kept with margin).
+constexpr int TILE_SMEM_MAX = 232448 - 2048;
 
-struct alignas(64) GramParams {
-  CUtensorMap map[2];  // span 0 / span 1 sources (column-major, box 16 rows x 8 cols)
-  int col0[2];         // first source column of each span
-  int ncols[2];        // loaded columns of each span
-  int lcols[2];        // columns of each span that are rows of the output (left operand)
-  int nbox[2];         // 8-column boxes of each span
-  int nboxes;          // nbox[0] + nbox[1]
-  int mt_out;          // boxes used as the left operand: nbox[0] or nboxes
-  int nt;              // n-tiles (set by the launcher)
-  int N;               // right-operand columns (<= 32)
-  int rcol[32];        // tile column of each right-operand column (-1: pad)
-  long n_rows;         // rows of this shard
-  long total_stages;   // set by the launcher
-  int stages;          // pipeline depth (set by the launcher)
-  double* partial;     // per-CTA (hi, lo) partials
+struct alignas(64) TileParams {
+  CUtensorMap map0[5];  // span-0 source, 3-D boxes {16, H, w}, w = 128/64/32/16/8 columns
+  CUtensorMap map1[2];  // span-1 source, w = 16/8 columns
+  int col0[2];          // first source column of each span
+  int units_span[2];    // 8-column units loaded per span
+  int lcols[2];         // columns of each span that are output rows (left operand)
+  int units;            // units_span[0] + units_span[1]
+  int mt_out;           // 8-column m-tiles used as the left operand (a prefix of the tile)
+  int nt;               // n-tiles (set by the launcher)
+  int N;                // right-operand columns (<= 32)
+  int rcol[32];         // tile column of each right-operand column (-1: pad)
+  long n_rows;          // rows of this shard
+  long total_stages;    // set by the launcher
+  int stages;           // pipeline depth
+  int H;                // 16-row blocks per stage (stage rows RS = 16 H)
+  double* partial;      // per-CTA (hi, lo) partials
   const DevStatus* status;
+  // K12: fused block update in front of the Gram (ignored by K1)
+  int upd_a, upd_b, kp, s, colA, colB;
+  const double* CA; int ldca; const double* TA;
+  const double* CB; int ldcb; const double* TB;
+  double* dstA; long lddA;
+  double* dstB; long lddB;
+  unsigned long long* phase;  // BGS_TILE_PROF: per-CTA cycle counters [grid][8] (or null)
+  int dbg;  // experiment mask (BGS_TILE_DBG): 1 no proxy fence, 2 no global stores,
+            // 4 no update MMAs, 8 no Gram MMAs, 16 no epilogue
 };
 
-// Per-CTA partials of one shard (p.partial already offset to this shard's first CTA).
-cudaError_t gram_partials_launch(GramParams& p, int grid, cudaStream_t st, int* launches);
+cudaError_t tile_launch(TileParams& p, bool upd, int grid, cudaStream_t st, int* launches);
+bool tile_fused_supported(int s, int kp, int mt_out);
+size_t tile_smem_bytes(int H, int stages, int units, bool upd);
 // Deterministic double-double sum over `ctas` partial slots -> compact M x N Gram
 // (M = lcols[0] + lcols[1]).
-cudaError_t gram_reduce_launch(const GramParams& p, int ctas, double* out, cudaStream_t st,
+cudaError_t gram_reduce_launch(const TileParams& p, int ctas, double* out, cudaStream_t st,
                                int* launches);
 int gram_n_tiles(int N);
 size_t gram_partial_doubles_per_cta(int mt_out, int N);

@@ -7,6 +7,9 @@
 //                 mt19937_64 stream is too slow; independent of the row sharding.
 //  residual     : sum of squares of X - Q R and of X (metrics.cpp:16-28), double-double
 //                 partials per CTA, for full-size verification on the device.
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -165,7 +168,7 @@ cudaError_t residual_launch(const double* x, long ldx, const double* q, long ldq
                             double* ws, double* out, int num_sms, cudaStream_t st) {
   const size_t smem = (size_t)m * RES_TILE * sizeof(double);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(residual_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ensure_smem(residual_kernel, smem);
   long grid = (n_rows + 255) / 256;
   if (grid > num_sms * 2) grid = num_sms * 2;
   if (grid < 1) grid = 1;
@@ -173,6 +176,17 @@ cudaError_t residual_launch(const double* x, long ldx, const double* q, long ldq
                                                 reinterpret_cast<double2*>(ws));
   dd_finish_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const double2*>(ws), (int)grid, out);
   return cudaGetLastError();
+}
+
+cudaError_t ensure_smem_impl(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[kernel];
+  if (bytes <= have) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 cudaError_t maxabs_launch(const double*, long, long, long, double*, double*, int, cudaStream_t) {

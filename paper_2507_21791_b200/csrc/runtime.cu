@@ -141,18 +141,23 @@ PFN_encodeTiled encoder() {
   return fn;
 }
 
-// Column-major rows x cols fp64 matrix, box = 16 rows x 8 columns, 128-byte swizzle.
-CUtensorMap make_map(const double* base, long rows, long cols, long ld) {
+// The {16 rows, row block, column} 3-D view of a column-major rows x cols fp64 matrix
+// used by the tile engine (gram.cu): box {16, H, w}, 128-byte swizzle.  Reads whole
+// 16-row blocks, so the storage must hold ceil(rows/16)*16 rows per column (ld >= that).
+CUtensorMap make_map3(const double* base, long rows, long cols, long ld, int H, int w) {
   CUtensorMap m;
   memset(&m, 0, sizeof m);
   if (rows <= 0 || cols <= 0) return m;
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1))
-    fail(BGS_E_DIMENSION, "device matrices need 16-byte aligned columns (even leading dimension)");
-  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-  cuuint32_t box[2] = {16, 8};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+  const long rb = (rows + 15) / 16;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1) || ld < rb * 16)
+    fail(BGS_E_DIMENSION,
+         "device matrices need 16-byte aligned columns and a leading dimension >= rows "
+         "rounded up to 16 (got rows %ld, ld %ld)", rows, ld);
+  cuuint64_t dims[3] = {16, (cuuint64_t)rb, (cuuint64_t)cols};
+  cuuint64_t strides[2] = {128, (cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[3] = {16, (cuuint32_t)H, (cuuint32_t)w};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -267,7 +272,15 @@ struct Shard {
   long ldx = 0;
   double* Q = nullptr;
   long ldq = 0;
-  CUtensorMap mapX, mapQ;
+  // tile-engine views: [H index: 0 -> H=2, 1 -> H=4][box width 128/64/32/16/8]
+  CUtensorMap mapX[2][5], mapQ[2][5];
+  void make_maps(long m) {
+    for (int hi = 0; hi < 2; ++hi)
+      for (int wi = 0; wi < 5; ++wi) {
+        mapX[hi][wi] = make_map3(X, rows, m, ldx, 2 << hi, 128 >> wi);
+        mapQ[hi][wi] = make_map3(Q, rows, m, ldq, 2 << hi, 128 >> wi);
+      }
+  }
   // TSQR leaf plan
   int leaf_base = 0, n_leaves = 0, bound_base = 0;
   long hmax = 0;
@@ -303,8 +316,19 @@ class Runner {
   DevStatus* status;
   int tsqr_L = 0;  // total leaves across local shards
 
+  bool no_fuse = false;
+  int tile_dbg = 0;
+  bool tile_prof = false;
+
   Runner(bgs_ctx* ctx, int v, long n_, long m_, long s_, int P_, bool nccl_, bgs_stats* st)
-      : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {}
+      : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {
+    const char* e = getenv("BGS_NO_FUSE");
+    no_fuse = e && *e && *e != '0';
+    const char* d = getenv("BGS_TILE_DBG");
+    tile_dbg = d ? atoi(d) : 0;
+    const char* tp = getenv("BGS_TILE_PROF");
+    tile_prof = tp && *tp && *tp != '0';
+  }
 
   // RAII bracket of one launch (or launch group) of a kernel class for the profiler.
   struct Prof {
@@ -359,10 +383,7 @@ class Runner {
     c->scolB.ensure((size_t)(m + s) * s * sizeof(double));
     c->save.ensure((size_t)(m + s) * s * sizeof(double));
     for (DBuf* b : {&c->sdiag, &c->ydiag, &c->r1, &c->r2, &c->rtop}) b->ensure(ss * sizeof(double) + 64);
-    for (auto& x : sh) {
-      x.mapX = make_map(x.X, x.rows, m, x.ldx);
-      x.mapQ = make_map(x.Q, x.rows, m, x.ldq);
-    }
+    for (auto& x : sh) x.make_maps(m);
     // Gram partial slots: every shard's CTAs
     const int boxes_max = (int)((m + 2 * s + 7) / 8) + 2;
     const size_t per_cta = gram_partial_doubles_per_cta(boxes_max, std::min<long>(2 * s, 32));
@@ -404,7 +425,7 @@ class Runner {
 
   int grid_for(const Shard& x) const {
     const int per = std::max(1, c->sms / (int)sh.size());
-    const long stages = (x.rows + 15) / 16;
+    const long stages = (x.rows + 63) / 64;
     return (int)std::max<long>(1, std::min<long>(per, stages));
   }
   int grid_total() const {
@@ -413,45 +434,101 @@ class Runner {
     return g;
   }
 
-  // ---------------- K1 + reduction + (NCCL) allreduce ----------------
+  // ---------------- K1 / K12 + reduction + (NCCL) allreduce ----------------
+  // Fused block update carried in front of the Gram (K12); dst columns are Q columns.
+  struct Fuse {
+    bool a = false, b = false;
+    int kp = 0;
+    const double* CA = nullptr; int ldca = 0; const double* TA = nullptr; long dstA = 0;
+    const double* CB = nullptr; int ldcb = 0; const double* TB = nullptr; long dstB = 0;
+  };
+
   // Returns M (rows of the compact Gram written to c->G, ld = M).
   int gram(const GramSpec& sp, const char* label, bool count_sync = true,
-           bool do_allreduce = true) {
-    GramParams p;
+           bool do_allreduce = true, const Fuse* fz = nullptr) {
+    TileParams p;
     memset(&p, 0, sizeof p);
-    int nbox[2] = {0, 0}, lc[2] = {0, 0};
+    int units[2] = {0, 0}, lc[2] = {0, 0};
     for (int i = 0; i < sp.nspans; ++i) {
-      nbox[i] = (sp.sp[i].ncols + 7) / 8;
+      units[i] = (sp.sp[i].ncols + 7) / 8;
       lc[i] = sp.sp[i].lcols;
     }
     const bool span1_left = sp.nspans == 2 && lc[1] > 0;
     if (span1_left && lc[0] != sp.sp[0].ncols) fail(BGS_E_INTERNAL, "gram: bad left layout");
-    p.nbox[0] = nbox[0];
-    p.nbox[1] = nbox[1];
-    p.nboxes = nbox[0] + nbox[1];
-    p.mt_out = span1_left ? p.nboxes : (lc[0] + 7) / 8;
+    p.units_span[0] = units[0];
+    p.units_span[1] = units[1];
+    p.units = units[0] + units[1];
+    p.mt_out = span1_left ? units[0] + (lc[1] + 7) / 8 : (lc[0] + 7) / 8;
     p.N = sp.N;
     for (int i = 0; i < 2; ++i) {
       p.col0[i] = sp.sp[i].col0;
-      p.ncols[i] = sp.sp[i].ncols;
       p.lcols[i] = lc[i];
     }
     for (int j = 0; j < 32; ++j)
-      p.rcol[j] = j < sp.N ? (sp.rspan[j] == 0 ? sp.rcol[j] : 8 * nbox[0] + sp.rcol[j]) : -1;
+      p.rcol[j] = j < sp.N ? (sp.rspan[j] == 0 ? sp.rcol[j] : 8 * units[0] + sp.rcol[j]) : -1;
     p.status = status;
+    p.dbg = tile_dbg;
+    if (tile_prof) {
+      c->metrics.ensure((size_t)256 * 16 * sizeof(unsigned long long) + 64);
+      p.phase = reinterpret_cast<unsigned long long*>(c->metrics.p);
+    }
+    const bool upd = fz != nullptr;
+    if (upd) {
+      if (!tile_fused_supported((int)s, fz->kp, p.mt_out) || sp.N > 8)
+        fail(BGS_E_INTERNAL, "gram: fused update not supported for this shape");
+      p.upd_a = fz->a;
+      p.upd_b = fz->b;
+      p.kp = fz->kp;
+      p.s = (int)s;
+      p.colA = fz->kp;
+      p.colB = 8 * units[0];
+      p.CA = fz->CA; p.ldca = fz->ldca; p.TA = fz->TA;
+      p.CB = fz->CB; p.ldcb = fz->ldcb; p.TB = fz->TB;
+    }
+    // Tallest stage (longest contiguous run per column) that keeps >= 3 (H=4) or >= 2
+    // (H=2) stages in flight within the CTA's shared memory.
+    int H = 0, S = 0;
+    for (int h : {4, 2}) {
+      const size_t one = tile_smem_bytes(h, 1, p.units, upd) - tile_smem_bytes(h, 0, p.units, upd);
+      const size_t fixed = tile_smem_bytes(h, 0, p.units, upd);
+      const int smax = (int)((TILE_SMEM_MAX - fixed) / one);
+      if (smax >= (h == 4 ? 3 : 2)) {
+        H = h;
+        S = std::min(smax, 8);
+        break;
+      }
+    }
+    if (!H) fail(BGS_E_CONFIG, "gram: a %d-column tile does not fit in shared memory", 8 * p.units);
+    p.H = H;
+    p.stages = S;
+    const int hi = H == 4 ? 1 : 0;
     const int M = lc[0] + (span1_left ? lc[1] : 0);
     const size_t per_cta = gram_partial_doubles_per_cta(p.mt_out, p.N);
     int cta_base = 0;
+    double flops_upd = 0.0, bytes_upd = 0.0;
     for (auto& x : sh) {
       const int grid = grid_for(x);
       if (x.rows > 0) {
-        p.map[0] = sp.sp[0].src == SX ? x.mapX : x.mapQ;
-        if (sp.nspans == 2) p.map[1] = sp.sp[1].src == SX ? x.mapX : x.mapQ;
+        for (int wi = 0; wi < 5; ++wi)
+          p.map0[wi] = sp.sp[0].src == SX ? x.mapX[hi][wi] : x.mapQ[hi][wi];
+        if (sp.nspans == 2)
+          for (int wi = 0; wi < 2; ++wi)
+            p.map1[wi] = sp.sp[1].src == SX ? x.mapX[hi][3 + wi] : x.mapQ[hi][3 + wi];
         p.n_rows = x.rows;
         p.partial = c->partial.d() + per_cta * cta_base;
-        Prof pr(c, "gram", 8.0 * x.rows * (sp.sp[0].ncols + (sp.nspans == 2 ? sp.sp[1].ncols : 0)),
-                2.0 * x.rows * (double)(lc[0] + (span1_left ? lc[1] : 0)) * sp.N);
-        CUDA_OK(gram_partials_launch(p, grid, c->stream, &c->launches));
+        if (upd) {
+          p.dstA = x.Q + (size_t)fz->dstA * x.ldq;
+          p.lddA = x.ldq;
+          p.dstB = x.Q + (size_t)fz->dstB * x.ldq;
+          p.lddB = x.ldq;
+          const int nout = (fz->a ? 1 : 0) + (fz->b ? 1 : 0);
+          bytes_upd = 8.0 * x.rows * s * nout;  // the written blocks
+          flops_upd = 2.0 * x.rows * (double)fz->kp * s * nout;
+        }
+        const double bytes = 8.0 * x.rows * (sp.sp[0].ncols + (sp.nspans == 2 ? sp.sp[1].ncols : 0));
+        Prof pr(c, upd ? "fused_update_gram" : "gram", bytes + bytes_upd,
+                2.0 * x.rows * (double)M * sp.N + flops_upd);
+        CUDA_OK(tile_launch(p, upd, grid, c->stream, &c->launches));
       } else {
         CUDA_OK(cudaMemsetAsync(c->partial.d() + per_cta * cta_base, 0,
                                 per_cta * grid * sizeof(double), c->stream));
@@ -588,7 +665,7 @@ class Runner {
     g.sp[1] = {src1, col1, n1, l1};
     return g;
   }
-  void set_right(GramSpec& g, int span, int col, int cnt) {
+  static void add_right(GramSpec& g, int span, int col, int cnt) {
     for (int j = 0; j < cnt; ++j) {
       g.rspan[g.N + j] = span;
       g.rcol[g.N + j] = col + j;
@@ -601,7 +678,46 @@ class Runner {
   // q = 1 (bcgs.cpp:83-90)
   void single_block() { tsqr(SX, 0, 0, Rd(), (int)m, "reduce_factor_tree:tsqr"); }
 
-  // onesync_impl (bcgs.cpp:233-369)
+  // Can the block update producing the left operand of `g` be fused in front of it?
+  bool fuse_ok(const GramSpec& g, int kp) const {
+    if (no_fuse || s > 4 || g.N > 8) return false;
+    int units = 0;
+    for (int i = 0; i < g.nspans; ++i) units += (g.sp[i].ncols + 7) / 8;
+    const bool span1_left = g.nspans == 2 && g.sp[1].lcols > 0;
+    const int mt_out = span1_left ? (g.sp[0].ncols + 7) / 8 + (g.sp[1].lcols + 7) / 8
+                                  : (g.sp[0].lcols + 7) / 8;
+    return tile_fused_supported((int)s, kp, mt_out) &&
+           tile_smem_bytes(2, 2, units, true) <= (size_t)TILE_SMEM_MAX;
+  }
+
+  // Gram of one-sync step j over [Q_{1:j} U_j (X_{j+1})] when U_j already sits in Q
+  // block j (unfused layout; fused_gram:wide / :final, bcgs.cpp:303-319).
+  GramSpec onesync_spec_unfused(int mode, long j) const {
+    const int si = (int)s, kp = (int)(j * s);
+    GramSpec g;
+    if (j + 1 < q) {
+      g = spec2(SQ, 0, kp + si, kp + si, SX, kp + si, si, mode == OS_PYTH ? si : 0);
+      add_right(g, 0, kp, si);
+      add_right(g, 1, 0, si);
+    } else {
+      g = spec1(SQ, 0, kp + si, kp + si);
+      add_right(g, 0, kp, si);
+    }
+    return g;
+  }
+  // The same Gram on the tile of a fused update: Q_{1:j} in span 0, [X_j -> U_j, X_{j+1}]
+  // in span 1 (U_j produced in place by the update).
+  GramSpec onesync_spec_fused(int mode, long j) const {
+    const int si = (int)s, kp = (int)(j * s);
+    const bool wide = j + 1 < q;
+    GramSpec g = spec2(SQ, 0, kp, kp, SX, kp, wide ? 2 * si : si,
+                       (wide && mode == OS_PYTH) ? 2 * si : si);
+    add_right(g, 1, 0, si);
+    if (wide) add_right(g, 1, si, si);
+    return g;
+  }
+
+  // onesync_impl (bcgs.cpp:233-369); modes PythChol (P-1S), SkipNorm (I+1S), TsqrPath (P-2S)
   void onesync(int mode, int kappa_power) {
     if (q == 1) return single_block();
     const int si = (int)s;
@@ -609,46 +725,52 @@ class Runner {
     double* scol_nxt = c->scolB.d();
     double* sdiag = c->sdiag.d();
     double* ydiag = c->ydiag.d();
+    const bool fusable = mode != OS_TSQR;
+    int M;
     // ---- prologue: TSQR(X_1) with the first Gram in the same rendezvous ----
     {
       const int lc = mode == OS_PYTH ? 2 * si : si;
       GramSpec g = spec1(SX, 0, 2 * si, lc);
-      set_right(g, 0, si, si);
-      const int M = gram(g, "", /*count_sync=*/false, /*do_allreduce=*/false);
-      tsqr(SX, 0, 0, c->rtop.d(), si, "reduce_factor_tree:prologue", (long)M * si, c->G.d());
+      add_right(g, 0, si, si);
+      const int M0 = gram(g, "", /*count_sync=*/false, /*do_allreduce=*/false);
+      tsqr(SX, 0, 0, c->rtop.d(), si, "reduce_factor_tree:prologue", (long)M0 * si, c->G.d());
       SmallParams sp;
       memset(&sp, 0, sizeof sp);
       sp.mode = SM_ONESYNC_PROLOGUE;
       sp.os_mode = mode;
       sp.kappa_power = kappa_power;
-      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+      sp.G = c->G.d(); sp.ldg = M0; sp.gm = M0; sp.gn = si;
       sp.rtop = c->rtop.d(); sp.ldrtop = si;
       sp.scol_next = scol_cur; sp.ld_scol_next = si;
       sp.sdiag = sdiag;
       small(sp);
-      Upd u;
-      u.kp = si;
-      u.has_b = true;
-      u.srcB = SX; u.colB = si; u.dstB = si;
-      u.CB = scol_cur; u.ldcb = si;
-      u.TB = mode == OS_PYTH ? sdiag : nullptr;
-      update(u);
-      if (mode == OS_TSQR) tsqr(SQ, si, si, sdiag, si, "reduce_factor_tree:tsqr");
+      // U_2 = (X_2 - Q_1 S_12) S_22^{-1}, then the Gram of step 1 (fused when possible)
+      const char* lab = q > 2 ? "fused_gram:wide" : "fused_gram:final";
+      GramSpec gf = onesync_spec_fused(mode, 1);
+      if (fusable && fuse_ok(gf, si)) {
+        Fuse fz;
+        fz.b = true;
+        fz.kp = si;
+        fz.CB = scol_cur; fz.ldcb = si;
+        fz.TB = mode == OS_PYTH ? sdiag : nullptr;
+        fz.dstB = si;
+        M = gram(gf, lab, true, true, &fz);
+      } else {
+        Upd u;
+        u.kp = si;
+        u.has_b = true;
+        u.srcB = SX; u.colB = si; u.dstB = si;
+        u.CB = scol_cur; u.ldcb = si;
+        u.TB = mode == OS_PYTH ? sdiag : nullptr;
+        update(u);
+        if (mode == OS_TSQR) tsqr(SQ, si, si, sdiag, si, "reduce_factor_tree:tsqr");
+        M = gram(onesync_spec_unfused(mode, 1), lab);
+      }
     }
     // ---- block steps ----
     for (long k = 1; k < q; ++k) {
       const int kp = (int)(k * s);
       const bool has_next = k + 1 < q;
-      GramSpec g;
-      if (has_next) {
-        g = spec2(SQ, 0, kp + si, kp + si, SX, kp + si, si, mode == OS_PYTH ? si : 0);
-        set_right(g, 0, kp, si);
-        set_right(g, 1, 0, si);
-      } else {
-        g = spec1(SQ, 0, kp + si, kp + si);
-        set_right(g, 0, kp, si);
-      }
-      const int M = gram(g, has_next ? "fused_gram:wide" : "fused_gram:final");
       SmallParams sp;
       memset(&sp, 0, sizeof sp);
       sp.mode = SM_ONESYNC_STEP;
@@ -657,27 +779,51 @@ class Runner {
       sp.kp = kp;
       sp.has_next = has_next;
       sp.kappa_power = kappa_power;
-      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = g.N;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = has_next ? 2 * si : si;
       sp.scol_prev = scol_cur; sp.ld_scol_prev = kp;
       sp.scol_next = scol_nxt; sp.ld_scol_next = kp + si;
       sp.sdiag = sdiag;
       sp.ydiag = ydiag;
       small(sp);
-      Upd u;
-      u.kp = kp;
-      u.has_a = true;
-      u.srcA = SQ; u.colA = kp; u.dstA = kp;
-      u.CA = c->G.d(); u.ldca = M; u.TA = ydiag;
-      if (has_next) {
+      if (!has_next) {
+        // Q_q = (U_q - Q_{1:q-1} Y) Y_qq^{-1}  (bcgs.cpp:329-331)
+        Upd u;
+        u.kp = kp;
+        u.has_a = true;
+        u.srcA = SQ; u.colA = kp; u.dstA = kp;
+        u.CA = c->G.d(); u.ldca = M; u.TA = ydiag;
+        update(u);
+        break;
+      }
+      // Q_k = (U_k - Q_{1:k} Y) Y_kk^{-1}; U_{k+1} = (X_{k+1} - Q_{1:k+1} [Z; S2]) S^{-1};
+      // then the Gram of step k+1 — one pass over Q_{1:k} when fused.
+      const char* lab = k + 2 < q ? "fused_gram:wide" : "fused_gram:final";
+      GramSpec gf = onesync_spec_fused(mode, k + 1);
+      gf.sp[0].ncols = gf.sp[0].lcols = kp + si;  // span 0 = [Q_{1:k} | U_k -> Q_k]
+      // (span 1 still starts at X block k+1)
+      if (fusable && fuse_ok(gf, kp)) {
+        Fuse fz;
+        fz.a = fz.b = true;
+        fz.kp = kp;
+        fz.CA = c->G.d(); fz.ldca = M; fz.TA = ydiag; fz.dstA = kp;
+        fz.CB = scol_nxt; fz.ldcb = kp + si; fz.TB = mode == OS_PYTH ? sdiag : nullptr;
+        fz.dstB = kp + si;
+        M = gram(gf, lab, true, true, &fz);
+      } else {
+        Upd u;
+        u.kp = kp;
+        u.has_a = true;
+        u.srcA = SQ; u.colA = kp; u.dstA = kp;
+        u.CA = c->G.d(); u.ldca = M; u.TA = ydiag;
         u.has_b = true;
         u.cb_has_a = true;
         u.srcB = SX; u.colB = kp + si; u.dstB = kp + si;
         u.CB = scol_nxt; u.ldcb = kp + si;
         u.TB = mode == OS_PYTH ? sdiag : nullptr;
+        update(u);
+        if (mode == OS_TSQR) tsqr(SQ, kp + si, kp + si, sdiag, si, "reduce_factor_tree:tsqr");
+        M = gram(onesync_spec_unfused(mode, k + 1), lab);
       }
-      update(u);
-      if (!has_next) break;
-      if (mode == OS_TSQR) tsqr(SQ, kp + si, kp + si, sdiag, si, "reduce_factor_tree:tsqr");
       std::swap(scol_cur, scol_nxt);
     }
   }
@@ -687,12 +833,12 @@ class Runner {
     if (q == 1) return single_block();
     const int si = (int)s;
     tsqr(SX, 0, 0, Rd(), (int)m, "reduce_factor_tree:tsqr");
+    // [S; T] = [Q_1 X_2]^T X_2
+    GramSpec g0 = spec2(SQ, 0, si, si, SX, si, si, si);
+    add_right(g0, 1, 0, si);
+    int M = gram(g0, "fused_gram:proj");
     for (long k = 1; k < q; ++k) {
       const int kp = (int)(k * s);
-      // [Q_{1:k} | X_k]: two spans; the reduction drops the tile padding between them
-      GramSpec g = spec2(SQ, 0, kp, kp, SX, kp, si, si);
-      set_right(g, 1, 0, si);
-      int M = gram(g, "fused_gram:proj");
       SmallParams sp;
       memset(&sp, 0, sizeof sp);
       sp.mode = SM_PIPI_PROJ;
@@ -701,15 +847,26 @@ class Runner {
       sp.save = c->save.d(); sp.ldsave = kp;
       sp.sdiag = c->sdiag.d();
       small(sp);
-      Upd u;
-      u.kp = kp;
-      u.has_a = true;
-      u.srcA = SX; u.colA = kp; u.dstA = kp;
-      u.CA = c->save.d(); u.ldca = kp; u.TA = c->sdiag.d();
-      update(u);
-      GramSpec g2 = spec1(SQ, 0, kp + si, kp + si);
-      set_right(g2, 0, kp, si);
-      M = gram(g2, "fused_gram:reproj");
+      // U = (X_k - Q S) S_kk^{-1}, then [Y; Omega] = [Q U]^T U  (bcgs.cpp:196-204)
+      GramSpec gr = spec2(SQ, 0, kp, kp, SX, kp, si, si);
+      add_right(gr, 1, 0, si);
+      if (fuse_ok(gr, kp)) {
+        Fuse fz;
+        fz.b = true;
+        fz.kp = kp;
+        fz.CB = c->save.d(); fz.ldcb = kp; fz.TB = c->sdiag.d(); fz.dstB = kp;
+        M = gram(gr, "fused_gram:reproj", true, true, &fz);
+      } else {
+        Upd u;
+        u.kp = kp;
+        u.has_a = true;
+        u.srcA = SX; u.colA = kp; u.dstA = kp;
+        u.CA = c->save.d(); u.ldca = kp; u.TA = c->sdiag.d();
+        update(u);
+        GramSpec g2 = spec1(SQ, 0, kp + si, kp + si);
+        add_right(g2, 0, kp, si);
+        M = gram(g2, "fused_gram:reproj");
+      }
       memset(&sp, 0, sizeof sp);
       sp.mode = SM_PIPI_REPROJ;
       sp.k = (int)k; sp.kp = kp; sp.kappa_power = 2;
@@ -718,12 +875,30 @@ class Runner {
       sp.sdiag = c->sdiag.d();
       sp.ydiag = c->ydiag.d();
       small(sp);
+      // Q_k = (U - Q Y) Y_kk^{-1}, then the next step's [Q X_{k+1}]^T X_{k+1}
+      if (k + 1 < q) {
+        GramSpec gp = spec2(SQ, 0, kp + si, kp + si, SX, kp + si, si, si);
+        add_right(gp, 1, 0, si);
+        if (fuse_ok(gp, kp)) {
+          Fuse fz;
+          fz.a = true;
+          fz.kp = kp;
+          fz.CA = c->G.d(); fz.ldca = M; fz.TA = c->ydiag.d(); fz.dstA = kp;
+          M = gram(gp, "fused_gram:proj", true, true, &fz);
+          continue;
+        }
+      }
       Upd u2;
       u2.kp = kp;
       u2.has_a = true;
       u2.srcA = SQ; u2.colA = kp; u2.dstA = kp;
       u2.CA = c->G.d(); u2.ldca = M; u2.TA = c->ydiag.d();
       update(u2);
+      if (k + 1 < q) {
+        GramSpec gp = spec2(SQ, 0, kp + si, kp + si, SX, kp + si, si, si);
+        add_right(gp, 1, 0, si);
+        M = gram(gp, "fused_gram:proj");
+      }
     }
   }
 
@@ -735,7 +910,7 @@ class Runner {
     for (long k = 1; k < q; ++k) {
       const int kp = (int)(k * s);
       GramSpec g = spec2(SQ, 0, kp, kp, SX, kp, si, 0);
-      set_right(g, 1, 0, si);
+      add_right(g, 1, 0, si);
       int M = gram(g, "fused_gram:proj1");
       SmallParams sp;
       memset(&sp, 0, sizeof sp);
@@ -752,7 +927,7 @@ class Runner {
       update(u);
       tsqr(SQ, kp, kp, c->r1.d(), si, "reduce_factor_tree:tsqr");
       GramSpec g2 = spec1(SQ, 0, kp + si, kp);
-      set_right(g2, 0, kp, si);
+      add_right(g2, 0, kp, si);
       M = gram(g2, "fused_gram:proj2");
       Upd u2;
       u2.kp = kp;
@@ -764,7 +939,7 @@ class Runner {
       memset(&sp, 0, sizeof sp);
       sp.mode = SM_IRO_FINISH;
       sp.k = (int)k; sp.kp = kp;
-      sp.G = c->G.d(); sp.ldg = M; sp.gm = 0; sp.gn = 0;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
       sp.aux1 = c->save.d(); sp.ldaux1 = kp;
       sp.aux2 = c->r1.d(); sp.ldaux2 = si;
       sp.rtop = c->r2.d(); sp.ldrtop = si;
@@ -772,7 +947,27 @@ class Runner {
     }
   }
 
+  void dump_phase_profile() {
+    if (!tile_prof) return;
+    std::vector<unsigned long long> h(256 * 16);
+    cudaMemcpy(h.data(), c->metrics.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    double tot[16] = {0};
+    for (int b = 0; b < 256; ++b)
+      for (int i = 0; i < 16; ++i) tot[i] += (double)h[b * 16 + i];
+    const double st = tot[9] > 0 ? tot[9] : 1;
+    fprintf(stderr,
+            "[tile phases] stages %.0f | cycles per stage (thread 0): wait %.0f update %.0f "
+            "reduce %.0f epilogue %.0f gram %.0f fence+arrive %.0f refill %.0f (empty-wait %.0f) "
+            "flush %.0f | total %.0f\n",
+            tot[9], tot[0] / st, tot[1] / st, tot[2] / st, tot[3] / st, tot[4] / st, tot[6] / st,
+            tot[7] / st, tot[10] / st, tot[8] / st, tot[5] / st);
+  }
+
   void run() {
+    if (tile_prof) {
+      c->metrics.ensure((size_t)256 * 16 * sizeof(unsigned long long) + 64);
+      CUDA_OK(cudaMemsetAsync(c->metrics.p, 0, 256 * 16 * sizeof(unsigned long long), c->stream));
+    }
     setup();
     switch (variant) {
       case BGS_BCGSI_PLUS: iro(); break;
@@ -836,7 +1031,9 @@ void select_device(bgs_ctx* c) { CUDA_OK(cudaSetDevice(c->device)); }
 
 }  // namespace
 
-static long even_ld(long rows) { return std::max<long>(2, (rows + 1) & ~1L); }
+// Leading dimension of library-owned device buffers: rows rounded up to 32 (the tile
+// engine's TMA view reads whole 16-row blocks; 32 keeps 256-byte column alignment).
+static long even_ld(long rows) { return std::max<long>(32, (rows + 31) & ~31L); }
 
 // =====================================================================================
 // C ABI
@@ -1110,6 +1307,7 @@ int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaGetLastError());
     c->prof_resolve();
+    run.dump_phase_profile();
     run.check_status();
     if (h_r)
       CUDA_OK(cudaMemcpy2D(h_r, ldr * sizeof(double), c->R.p, m * sizeof(double), m * sizeof(double),
@@ -1190,8 +1388,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
     c->status.ensure(sizeof(DevStatus));
     run.status = reinterpret_cast<DevStatus*>(c->status.p);
     CUDA_OK(cudaMemsetAsync(run.status, 0, sizeof(DevStatus), c->stream));
-    run.sh[0].mapX = make_map(d_x, n_local, m, ldx);
-    run.sh[0].mapQ = make_map(d_q, n_local, m, ldq);
+    run.sh[0].make_maps(m);
     const size_t per_cta = gram_partial_doubles_per_cta((int)((m + 7) / 8) + 1, si);
     c->partial.ensure(per_cta * sizeof(double) * (size_t)run.grid_total() + 64);
     c->G.ensure((size_t)(m + 16) * 32 * sizeof(double) + 4096);
@@ -1199,7 +1396,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
     for (long j0 = 0; j0 < m; j0 += si) {
       const int nb = (int)std::min<long>(si, m - j0);
       GramSpec g = Runner::spec1(SQ, 0, (int)m, (int)m);
-      run.set_right(g, 0, (int)j0, nb);
+      run.add_right(g, 0, (int)j0, nb);
       run.gram(g, "", false, true);
       CUDA_OK(cudaMemcpyAsync(panel.data(), c->G.p, (size_t)m * nb * sizeof(double),
                               cudaMemcpyDeviceToHost, c->stream));
@@ -1334,9 +1531,12 @@ int bgs_gram(bgs_ctx* c, const double* a, long n, long ma, const double* b, long
     sh.rows = n;
     sh.Q = da.d(); sh.ldq = ld;
     sh.X = db.d(); sh.ldx = ld;
-    sh.mapQ = make_map(da.d(), n, ma, ld);
-    sh.mapX = make_map(db.d(), n, mb, ld);
     run.sh.push_back(sh);
+    for (int hi = 0; hi < 2; ++hi)
+      for (int wi = 0; wi < 5; ++wi) {
+        run.sh[0].mapQ[hi][wi] = make_map3(da.d(), n, ma, ld, 2 << hi, 128 >> wi);
+        run.sh[0].mapX[hi][wi] = make_map3(db.d(), n, mb, ld, 2 << hi, 128 >> wi);
+      }
     c->status.ensure(sizeof(DevStatus));
     run.status = reinterpret_cast<DevStatus*>(c->status.p);
     CUDA_OK(cudaMemsetAsync(run.status, 0, sizeof(DevStatus), c->stream));
@@ -1344,7 +1544,7 @@ int bgs_gram(bgs_ctx* c, const double* a, long n, long ma, const double* b, long
     c->partial.ensure(per_cta * sizeof(double) * (size_t)run.grid_total() + 64);
     c->G.ensure((size_t)ma * mb * sizeof(double) + 64);
     GramSpec g = Runner::spec2(SQ, 0, (int)ma, (int)ma, SX, 0, (int)mb, 0);
-    run.set_right(g, 1, 0, (int)mb);
+    run.add_right(g, 1, 0, (int)mb);
     run.gram(g, "", false, false);
     CUDA_OK(cudaMemcpyAsync(out, c->G.p, (size_t)ma * mb * sizeof(double), cudaMemcpyDeviceToHost,
                             c->stream));

@@ -33,13 +33,23 @@ struct Smem {
 };
 
 // out(i,j) = sum_r A(r,i) B(r,j), rows x s each; one warp per entry, fixed order.
-__device__ void cta_atb(const double* A, int lda, const double* B, int ldb, int rows, int s,
+__device__ __noinline__ void cta_atb(const double* A, int lda, const double* B, int ldb, int rows, int s,
                         double* out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = warp; e < s * s; e += kWarps) {
     const int i = e % s, j = e / s;
-    double acc = 0.0;
-    for (int r = lane; r < rows; r += 32) acc = fma(A[r + (size_t)i * lda], B[r + (size_t)j * ldb], acc);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double* Ai = A + (size_t)i * lda;
+    const double* Bj = B + (size_t)j * ldb;
+    int r = lane;
+    for (; r + 96 < rows; r += 128) {
+      a0 = fma(Ai[r], Bj[r], a0);
+      a1 = fma(Ai[r + 32], Bj[r + 32], a1);
+      a2 = fma(Ai[r + 64], Bj[r + 64], a2);
+      a3 = fma(Ai[r + 96], Bj[r + 96], a3);
+    }
+    for (; r < rows; r += 32) a0 = fma(Ai[r], Bj[r], a0);
+    double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) out[i + j * s] = acc;
@@ -48,14 +58,11 @@ __device__ void cta_atb(const double* A, int lda, const double* B, int ldb, int 
 
 // Upper Cholesky of the symmetrized a (s x s) into g; returns the 1-based failing pivot.
 // Thread-serial: s <= 16 (chol_factor, dense_kernels.cpp:54-87).
-__device__ int chol_serial(const double* a, int s, double* g) {
-  double sym[SMAX * SMAX];
-  for (int j = 0; j < s; ++j)
-    for (int i = 0; i < s; ++i) sym[i + j * s] = 0.5 * (a[i + j * s] + a[j + i * s]);
+__device__ __noinline__ int chol_serial(const double* a, int s, double* g) {
   for (int k = 0; k < s * s; ++k) g[k] = 0.0;
   for (int j = 0; j < s; ++j) {
     for (int i = 0; i <= j; ++i) {
-      double acc = sym[i + j * s];
+      double acc = 0.5 * (a[i + j * s] + a[j + i * s]);
       for (int k = 0; k < i; ++k) acc -= g[k + i * s] * g[k + j * s];
       if (i == j) {
         if (!(acc > 0.0)) return j + 1;
@@ -70,7 +77,7 @@ __device__ int chol_serial(const double* a, int s, double* g) {
 
 // W = G^{-T} B for upper G (s x s), B (s x s) (tri_solve_left_trans).  Returns 1-based
 // index of a zero diagonal entry (SingularError), else 0.
-__device__ int trsm_lt_serial(const double* g, int ldg_, const double* b, int ldb, int s,
+__device__ __noinline__ int trsm_lt_serial(const double* g, int ldg_, const double* b, int ldb, int s,
                               double* w) {
   for (int i = 0; i < s; ++i) {
     const double gii = g[i + i * ldg_];
@@ -94,22 +101,8 @@ __device__ void set_status(DevStatus* st, int code, int pivot, int block, int si
   }
 }
 
-// Non-finite scan of the reduced Gram (round_accumulators' NonFiniteError).
-__device__ bool gram_finite(const SmallParams& p, Smem& sh) {
-  if (threadIdx.x == 0) sh.flag = 0;
-  __syncthreads();
-  int bad = 0;
-  for (int e = threadIdx.x; e < p.gm * p.gn; e += kThreads) {
-    const int i = e % p.gm, j = e / p.gm;
-    if (!isfinite(p.G[i + (size_t)j * p.ldg])) bad = 1;
-  }
-  if (bad) atomicOr(&sh.flag, 1);
-  __syncthreads();
-  return sh.flag == 0;
-}
-
 // R(0:kp, k-block) = S + Y * Sd  (store_column_blocks of scol + multiply(ycol, sdiag))
-__device__ void r_column(const SmallParams& p, const double* Sc, int ldsc, const double* Y,
+__device__ __noinline__ void r_column(const SmallParams& p, const double* Sc, int ldsc, const double* Y,
                          int ldy, const double* Sd, int ldsd) {
   const int s = p.s, kp = p.kp;
   for (int e = threadIdx.x; e < kp * s; e += kThreads) {
@@ -121,7 +114,7 @@ __device__ void r_column(const SmallParams& p, const double* Sc, int ldsc, const
 }
 
 // R_kk = upper_product(a, b) (bcgs.cpp:35-49); lower triangle stays exact zero.
-__device__ void r_diag(const SmallParams& p, const double* a, const double* b) {
+__device__ __noinline__ void r_diag(const SmallParams& p, const double* a, const double* b) {
   const int s = p.s;
   for (int e = threadIdx.x; e < s * s; e += kThreads) {
     const int i = e % s, j = e / s;
@@ -134,22 +127,60 @@ __device__ void r_diag(const SmallParams& p, const double* a, const double* b) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p) {
+// Copies an r x c column-major global block into shared memory (ld = r) with one
+// coalesced pass: all loads of a thread are independent, so the L2 latency is paid once.
+__device__ __noinline__ void stage(const double* src, int ld, int r, int c, double* dst) {
+  for (int e = threadIdx.x; e < r * c; e += kThreads) dst[e] = src[(e % r) + (size_t)(e / r) * ld];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
   if (status_bad(p.status)) return;
   __shared__ Smem sh;
+  extern __shared__ double dyn[];
   const int s = p.s, kp = p.kp;
   const int tid = threadIdx.x;
+  // dynamic shared memory: [G gm x gn][scol_prev kp x s][scol_next (kp+s) x s]
+  double* gs = dyn;
+  double* sprev = gs + (size_t)p.gm * p.gn;
+  double* snext = sprev + (size_t)kp * s;
 
-  if (p.gm > 0 && !gram_finite(p, sh)) {
+  // ---- stage every input with one parallel pass ----
+  if (tid == 0) sh.flag = 0;
+  __syncthreads();
+  if (p.gm > 0) {
+    int bad = 0;
+    for (int e = tid; e < p.gm * p.gn; e += kThreads) {
+      const double v = p.G[(e % p.gm) + (size_t)(e / p.gm) * p.ldg];
+      gs[e] = v;
+      bad |= !isfinite(v);
+    }
+    if (bad) atomicOr(&sh.flag, 1);
+    p.G = gs;  // every mode below reads the Gram from shared memory
+    p.ldg = p.gm;
+  }
+  if (MODE == SM_ONESYNC_STEP) stage(p.scol_prev, p.ld_scol_prev, kp, s, sprev);
+  if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH) stage(p.aux1, p.ldaux1, kp, s, sprev);
+  for (int e = tid; e < s * s; e += kThreads) {
+    if (p.sdiag) sh.sdp[e] = p.sdiag[e];
+    if (MODE == SM_IRO_FINISH) {
+      sh.a[e] = p.aux2[(e % s) + (size_t)(e / s) * p.ldaux2];  // R1
+      sh.b[e] = p.rtop[(e % s) + (size_t)(e / s) * p.ldrtop];  // R2
+    }
+    if (MODE == SM_ONESYNC_PROLOGUE || MODE == SM_COPY_RBLOCK)
+      sh.b[e] = p.rtop[(e % s) + (size_t)(e / s) * p.ldrtop];  // root R
+  }
+  __syncthreads();
+  if (sh.flag) {
     if (tid == 0) set_status(p.status, ST_NON_FINITE, 0, p.k + 1, SITE_NONE, 0);
     return;
   }
 
-  switch (p.mode) {
+  switch (MODE) {
     case SM_COPY_RBLOCK: {
       for (int e = tid; e < s * s; e += kThreads) {
         const int i = e % s, j = e / s;
-        p.R[(kp + i) + (size_t)(kp + j) * p.ldr] = i <= j ? p.rtop[i + j * p.ldrtop] : 0.0;
+        p.R[(kp + i) + (size_t)(kp + j) * p.ldr] = i <= j ? sh.b[e] : 0.0;
       }
       return;
     }
@@ -157,10 +188,10 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
       // R(0,0) = R00; scol = R00^{-T} (X1^T X2)  (bcgs.cpp:264-276)
       for (int e = tid; e < s * s; e += kThreads) {
         const int i = e % s, j = e / s;
-        p.R[i + (size_t)j * p.ldr] = i <= j ? p.rtop[i + j * p.ldrtop] : 0.0;
+        p.R[i + (size_t)j * p.ldr] = i <= j ? sh.b[e] : 0.0;
       }
       if (tid == 0) {
-        sh.pivot = trsm_lt_serial(p.rtop, p.ldrtop, p.G, p.ldg, s, sh.a);
+        sh.pivot = trsm_lt_serial(sh.b, s, p.G, p.ldg, s, sh.a);
         if (sh.pivot) set_status(p.status, ST_SINGULAR, sh.pivot, 1, SITE_NONE, 0);
       }
       __syncthreads();
@@ -169,11 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         p.scol_next[(e % s) + (size_t)(e / s) * p.ld_scol_next] = sh.a[e];
       if (p.os_mode == OS_PYTH) {
         // S_diag = chol(T2 - scol^T scol)  (bcgs.cpp:280-287)
-        cta_atb(sh.a, s, sh.a, s, s, s, sh.b);
+        cta_atb(sh.a, s, sh.a, s, s, s, sh.c);
         __syncthreads();
         if (tid == 0) {
           for (int e = 0; e < s * s; ++e)
-            sh.c[e] = p.G[(s + e % s) + (size_t)(e / s) * p.ldg] - sh.b[e];
+            sh.c[e] = p.G[(s + e % s) + (size_t)(e / s) * p.ldg] - sh.c[e];
           const int piv = chol_serial(sh.c, s, sh.d);
           if (piv) set_status(p.status, ST_NOT_SPD, piv, 2, SITE_PROLOGUE_PYTH, p.kappa_power);
           for (int e = 0; e < s * s; ++e) p.sdiag[e] = sh.d[e];
@@ -186,7 +217,6 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     case SM_ONESYNC_STEP: {
       const double* Y = p.G;             // G[0:kp, 0:s]
       const double* Om = p.G + kp;       // G[kp:kp+s, 0:s]
-      for (int e = tid; e < s * s; e += kThreads) sh.sdp[e] = p.sdiag[e];
       // Y^T Y, then Y_diag = chol(Omega - Y^T Y)  (bcgs.cpp:321-327)
       cta_atb(Y, p.ldg, Y, p.ldg, kp, s, sh.a);
       __syncthreads();
@@ -195,12 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         sh.pivot = chol_serial(sh.c, s, sh.d);
         if (sh.pivot)
           set_status(p.status, ST_NOT_SPD, sh.pivot, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
-        for (int e = 0; e < s * s; ++e) p.ydiag[e] = sh.d[e];
       }
       __syncthreads();
       if (sh.pivot) return;
+      for (int e = tid; e < s * s; e += kThreads) p.ydiag[e] = sh.d[e];
       // R column = scol + Y S_diag; R_kk = Y_diag S_diag  (bcgs.cpp:332-333)
-      r_column(p, p.scol_prev, p.ld_scol_prev, Y, p.ldg, sh.sdp, s);
+      r_column(p, sprev, kp, Y, p.ldg, sh.sdp, s);
       r_diag(p, sh.d, sh.sdp);
       if (!p.has_next) return;
       // S2 = Y_diag^{-T} (P - Y^T Z); scol = [Z; S2]  (bcgs.cpp:336-344)
@@ -215,22 +245,24 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
       }
       __syncthreads();
       if (sh.pivot) return;
-      for (int e = tid; e < (kp + s) * s; e += kThreads) {
-        const int i = e % (kp + s), j = e / (kp + s);
-        p.scol_next[i + (size_t)j * p.ld_scol_next] =
-            i < kp ? Z[i + (size_t)j * p.ldg] : sh.c[(i - kp) + j * s];
+      const int kn = kp + s;
+      for (int e = tid; e < kn * s; e += kThreads) {
+        const int i = e % kn, j = e / kn;
+        const double v = i < kp ? Z[i + (size_t)j * p.ldg] : sh.c[(i - kp) + j * s];
+        snext[e] = v;
+        p.scol_next[i + (size_t)j * p.ld_scol_next] = v;
       }
       if (p.os_mode == OS_PYTH) {
         __syncthreads();
         // S_diag = chol(T - scol^T scol)  (bcgs.cpp:352-359)
-        cta_atb(p.scol_next, p.ld_scol_next, p.scol_next, p.ld_scol_next, kp + s, s, sh.a);
+        cta_atb(snext, kn, snext, kn, kn, s, sh.a);
         __syncthreads();
         if (tid == 0) {
           const double* T = p.G + kp + s + (size_t)s * p.ldg;
           for (int e = 0; e < s * s; ++e) sh.b[e] = T[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
-          const int piv = chol_serial(sh.b, s, sh.d);
+          const int piv = chol_serial(sh.b, s, sh.c);
           if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 2, SITE_FIRST_PASS, p.kappa_power);
-          for (int e = 0; e < s * s; ++e) p.sdiag[e] = sh.d[e];
+          for (int e = 0; e < s * s; ++e) p.sdiag[e] = sh.c[e];
         }
       } else if (p.os_mode == OS_SKIP) {
         for (int e = tid; e < s * s; e += kThreads) p.sdiag[e] = (e % s == e / s) ? 1.0 : 0.0;
@@ -253,7 +285,6 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     }
     case SM_PIPI_REPROJ: {
       // [Y; Omega] = [Q U]^T U -> Y_diag = chol(Omega - Y^T Y); R column  (bcgs.cpp:199-216)
-      for (int e = tid; e < s * s; e += kThreads) sh.sdp[e] = p.sdiag[e];
       cta_atb(p.G, p.ldg, p.G, p.ldg, kp, s, sh.a);
       __syncthreads();
       if (tid == 0) {
@@ -261,11 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
         sh.pivot = chol_serial(sh.b, s, sh.d);
         if (sh.pivot)
           set_status(p.status, ST_NOT_SPD, sh.pivot, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
-        for (int e = 0; e < s * s; ++e) p.ydiag[e] = sh.d[e];
       }
       __syncthreads();
       if (sh.pivot) return;
-      r_column(p, p.aux1, p.ldaux1, p.G, p.ldg, sh.sdp, s);
+      for (int e = tid; e < s * s; e += kThreads) p.ydiag[e] = sh.d[e];
+      r_column(p, sprev, kp, p.G, p.ldg, sh.sdp, s);
       r_diag(p, sh.d, sh.sdp);
       return;
     }
@@ -276,12 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
     }
     case SM_IRO_FINISH: {
       // R column = S1 + S2 R1; R_kk = R2 R1  (bcgs.cpp:162-164)
-      for (int e = tid; e < s * s; e += kThreads) {
-        sh.a[e] = p.aux2[(e % s) + (size_t)(e / s) * p.ldaux2];  // R1
-        sh.b[e] = p.rtop[(e % s) + (size_t)(e / s) * p.ldrtop];  // R2
-      }
-      __syncthreads();
-      r_column(p, p.aux1, p.ldaux1, p.G, p.ldg, sh.a, s);
+      r_column(p, sprev, kp, p.G, p.ldg, sh.a, s);
       r_diag(p, sh.b, sh.a);
       return;
     }
@@ -292,7 +318,28 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(const SmallParams p)
 
 cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches) {
   if (p.s < 1 || p.s > SMAX) return cudaErrorInvalidValue;
-  small_kernel<<<1, kThreads, 0, st>>>(p);
+  const size_t smem =
+      ((size_t)(p.gm > 0 ? p.gm * p.gn : 0) + (size_t)p.kp * p.s + (size_t)(p.kp + p.s) * p.s) *
+      sizeof(double);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaSuccess;
+#define BGS_SMALL_CASE(M)                      \
+  case M:                                      \
+    e = ensure_smem(small_kernel<M>, smem);    \
+    if (e != cudaSuccess) return e;            \
+    small_kernel<M><<<1, kThreads, smem, st>>>(p); \
+    break;
+  switch (p.mode) {
+    BGS_SMALL_CASE(SM_ONESYNC_PROLOGUE)
+    BGS_SMALL_CASE(SM_ONESYNC_STEP)
+    BGS_SMALL_CASE(SM_PIPI_PROJ)
+    BGS_SMALL_CASE(SM_PIPI_REPROJ)
+    BGS_SMALL_CASE(SM_IRO_SAVE)
+    BGS_SMALL_CASE(SM_IRO_FINISH)
+    BGS_SMALL_CASE(SM_COPY_RBLOCK)
+    default: return cudaErrorInvalidValue;
+  }
+#undef BGS_SMALL_CASE
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

@@ -399,8 +399,7 @@ cudaError_t tsqr_leaf_launch(const double* src, long lds, double* dst, long ldd,
                              const long* d_bounds, int L, long hmax, int s, double* rleaf,
                              const DevStatus* status, cudaStream_t st, int* launches) {
   const size_t smem = (size_t)2 * (hmax > 0 ? hmax : 1) * s * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(tsqr_leaf_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(tsqr_leaf_kernel, smem);
   if (e != cudaSuccess) return e;
   tsqr_leaf_kernel<<<L, kLeafThreads, smem, st>>>(src, lds, dst, ldd, d_bounds, s, rleaf, status);
   if (launches) *launches += 1;

@@ -148,15 +148,15 @@ static cudaError_t launch_s(const UpdateParams& p, int grid, size_t smem, cudaSt
   const bool ha = p.has_a, hb = p.has_b;
   if (ha && hb) {
     auto k = update_kernel<S, RPT, true, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(k, smem);
     k<<<grid, 256, smem, st>>>(p);
   } else if (ha) {
     auto k = update_kernel<S, RPT, true, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(k, smem);
     k<<<grid, 256, smem, st>>>(p);
   } else if (hb) {
     auto k = update_kernel<S, RPT, false, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(k, smem);
     k<<<grid, 256, smem, st>>>(p);
   } else {
     return cudaSuccess;
