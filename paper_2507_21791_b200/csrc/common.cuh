@@ -155,6 +155,9 @@ BGS_DEV double lds64(uint32_t addr) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
   return v;
 }
+BGS_DEV void sts128(uint32_t addr, double a, double b) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
 BGS_DEV void sts64(uint32_t addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
@@ -166,6 +169,78 @@ BGS_DEV void two_sum(double a, double b, double& s, double& e) {
   s = __dadd_rn(a, b);
   double bb = __dsub_rn(s, a);
   e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// ---------------------------------------------------------------------------------
+// Stage layout of the tile kernels (gram.cu, k12.cu): a stage is 16H rows x the tile's
+// columns; 128-byte line L = H*col + h holds rows 16h..16h+15 of tile column col, its
+// 16-byte chunk j stored at chunk j ^ (L & 7) (TMA SWIZZLE_128B of a {16, H, w} box).
+// ---------------------------------------------------------------------------------
+// byte offset of the 8-byte element (row r, tile column c) inside a stage
+template <int H>
+BGS_DEV uint32_t elem_off(int col, int r) {
+  const int line = H * col + (r >> 4);
+  const int chunk = ((r & 15) >> 1) ^ (line & 7);
+  return (uint32_t)(line * 128 + chunk * 16 + (r & 1) * 8);
+}
+
+// DMMA column-major fragment: rows 16h + 4kk + {0,1,2,3} of tile column `col`; odd-ii
+// lanes fetch the two chunks in swapped order so a quarter-warp hits 8 distinct chunks.
+template <int H>
+BGS_DEV void frag4(uint32_t stage, int col, int h, int kk, int odd, double (&v)[4]) {
+  const int line = H * col + h;
+  const uint32_t b = stage + (uint32_t)(line * 128);
+  const int c0 = (2 * kk + odd) ^ (line & 7), c1 = (2 * kk + 1 - odd) ^ (line & 7);
+  const double2 x0 = lds128(b + (uint32_t)(c0 << 4));
+  const double2 x1 = lds128(b + (uint32_t)(c1 << 4));
+  v[0] = odd ? x1.x : x0.x;
+  v[1] = odd ? x1.y : x0.y;
+  v[2] = odd ? x0.x : x1.x;
+  v[3] = odd ? x0.y : x1.y;
+}
+
+// ---------------------------------------------------------------------------------
+// Thread-block clusters / distributed shared memory
+// ---------------------------------------------------------------------------------
+BGS_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address -> the same offset in CTA `rank` of the cluster (shared::cluster)
+BGS_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(addr), "r"(rank));
+  return d;
+}
+// 16-byte store into a peer CTA's shared memory that completes `bytes` on the peer's
+// mbarrier (no separate fence / arrive needed on the sender side).
+BGS_DEV void st_async_v2f64(uint32_t remote_addr, double a, double b, uint32_t remote_bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+          remote_addr),
+      "d"(a), "d"(b), "r"(remote_bar)
+      : "memory");
+}
+BGS_DEV void cluster_sync_all() {
+  asm volatile(
+      "barrier.cluster.arrive.release.aligned;\n\t"
+      "barrier.cluster.wait.acquire.aligned;" ::
+          : "memory");
+}
+BGS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+// named barrier over `threads` threads (id 0 is __syncthreads)
+BGS_DEV void bar_named(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // Swizzled (CU_TENSOR_MAP_SWIZZLE_128B) byte offset of the 16-byte chunk `chunk`

@@ -50,28 +50,6 @@ struct Roles {
   static constexpr int WG = UPD ? 8 : 7;  // Gram warps
 };
 
-// byte offset of the 8-byte element (row r, tile column c) inside a stage
-template <int H>
-BGS_DEV uint32_t elem_off(int col, int r) {
-  const int line = H * col + (r >> 4);
-  const int chunk = ((r & 15) >> 1) ^ (line & 7);
-  return (uint32_t)(line * 128 + chunk * 16 + (r & 1) * 8);
-}
-
-// Gram fragment: rows 16h + 4kk + {0,1,2,3} of tile column `col`.
-template <int H>
-BGS_DEV void frag4(uint32_t stage, int col, int h, int kk, int odd, double (&v)[4]) {
-  const int line = H * col + h;
-  const uint32_t b = stage + (uint32_t)(line * 128);
-  const int c0 = (2 * kk + odd) ^ (line & 7), c1 = (2 * kk + 1 - odd) ^ (line & 7);
-  const double2 x0 = lds128(b + (uint32_t)(c0 << 4));
-  const double2 x1 = lds128(b + (uint32_t)(c1 << 4));
-  v[0] = odd ? x1.x : x0.x;
-  v[1] = odd ? x1.y : x0.y;
-  v[2] = odd ? x0.x : x1.x;
-  v[3] = odd ? x0.y : x1.y;
-}
-
 // Named barrier over the warps that run the stage loop (all 8 in K12, 0-6 in K1).
 template <int NWARPS>
 BGS_DEV void bar_warps() {

@@ -61,6 +61,44 @@ cudaError_t gram_reduce_launch(const TileParams& p, int ctas, double* out, cudaS
 int gram_n_tiles(int N);
 size_t gram_partial_doubles_per_cta(int mt_out, int N);
 
+// ---------------- K12c: cluster-split fused update + Gram (k12.cu) ----------------
+// A CTA pair shares each 32-row stage: rank r loads its own span-0 units plus the
+// extra (A-block) units it needs and all of span 1; the partial block update is
+// exchanged through distributed shared memory.  s <= 4, N <= 8.
+struct alignas(64) SplitParams {
+  CUtensorMap map0[5];  // span 0, boxes {16, 2, w}, w = 128/64/32/16/8
+  CUtensorMap map1[2];  // span 1, w = 16/8
+  int col0[2];          // first source column of each span
+  int U0, U1;           // 8-column units of span 0 / span 1
+  int ncols0;           // columns of span 0 (all are output rows)
+  int lcols1;           // output-row columns of span 1 (rank 0 emits them)
+  int s1_left;          // ceil(lcols1 / 8)
+  int own_u0[2], own_n[2];  // per cluster rank: owned span-0 units
+  int ext_u0[2], ext_n[2];  // per cluster rank: extra span-0 units (the A block)
+  int slot_units;       // max local units over the two ranks
+  int mt_out;           // global 8-column output tiles (U0 + s1_left)
+  int N;                // right-operand columns (<= 8), all in span 1
+  int rcol1[8];         // span-1 column of each right-operand column (-1: pad)
+  long n_rows;
+  long total_stages;    // 32-row stages of the shard
+  int stages;           // ring depth
+  int kw, mtw;          // k-steps / output tiles per warp (planned; selects the instance)
+  int upd_a, upd_b, kp, s;
+  const double* CA; int ldca; const double* TA;
+  const double* CB; int ldcb; const double* TB;
+  double* dstA; long lddA;
+  double* dstB; long lddB;
+  double* partial;      // (hi, lo) partials, one slot per (cluster, consumer group)
+  const DevStatus* status;
+  unsigned long long* phase;
+  int dbg;
+};
+// Plans the rank split for a fused Gram of the given shape; false when K12c does not
+// apply (then the caller uses tile_launch).  Fills own/ext ranges, slot_units, stages.
+bool k12_plan(SplitParams& p);
+size_t k12_smem_bytes(int stages, int slot_units);
+cudaError_t k12_launch(const SplitParams& p, int grid, cudaStream_t st, int* launches);
+
 // ---------------- K2: block update (update.cu) ----------------
 struct UpdateParams {
   long n_rows;

@@ -317,6 +317,7 @@ class Runner {
   int tsqr_L = 0;  // total leaves across local shards
 
   bool no_fuse = false;
+  bool no_k12c = false;
   int tile_dbg = 0;
   bool tile_prof = false;
 
@@ -324,6 +325,9 @@ class Runner {
       : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {
     const char* e = getenv("BGS_NO_FUSE");
     no_fuse = e && *e && *e != '0';
+    // K12c (cluster-split fused kernel) is opt-in until it beats the single-CTA K12
+    const char* e2 = getenv("BGS_K12C");
+    no_k12c = !(e2 && *e2 && *e2 != '0');
     const char* d = getenv("BGS_TILE_DBG");
     tile_dbg = d ? atoi(d) : 0;
     const char* tp = getenv("BGS_TILE_PROF");
@@ -443,6 +447,91 @@ class Runner {
     const double* CB = nullptr; int ldcb = 0; const double* TB = nullptr; long dstB = 0;
   };
 
+  // K12c (k12.cu): the fused update + Gram split over CTA pairs.  Returns -1 when the
+  // shape is not covered (the caller then uses the single-CTA tile engine).
+  int gram_split(const GramSpec& sp, const char* label, bool count_sync, bool do_allreduce,
+                 const Fuse& fz, const int units[2], const int lc[2]) {
+    if (sp.nspans != 2 || sp.N > 8 || lc[0] != sp.sp[0].ncols) return -1;
+    SplitParams p;
+    memset(&p, 0, sizeof p);
+    for (int j = 0; j < sp.N; ++j) {
+      if (sp.rspan[j] != 1) return -1;
+      p.rcol1[j] = sp.rcol[j];
+    }
+    for (int j = sp.N; j < 8; ++j) p.rcol1[j] = -1;
+    p.N = sp.N;
+    p.U0 = units[0];
+    p.U1 = units[1];
+    p.ncols0 = sp.sp[0].ncols;
+    p.lcols1 = lc[1];
+    p.col0[0] = sp.sp[0].col0;
+    p.col0[1] = sp.sp[1].col0;
+    p.upd_a = fz.a;
+    p.upd_b = fz.b;
+    p.kp = fz.kp;
+    p.s = (int)s;
+    p.CA = fz.CA; p.ldca = fz.ldca; p.TA = fz.TA;
+    p.CB = fz.CB; p.ldcb = fz.ldcb; p.TB = fz.TB;
+    p.status = status;
+    p.dbg = tile_dbg;
+    if (!k12_plan(p)) return -1;
+    for (auto& x : sh)
+      if (x.rows > 0 && grid_for(x) < 2) return -1;
+    if (tile_prof) {
+      c->metrics.ensure((size_t)512 * 16 * sizeof(unsigned long long) + 64);
+      p.phase = reinterpret_cast<unsigned long long*>(c->metrics.p) + 256 * 16;
+    }
+    const int M = lc[0] + lc[1];
+    const size_t per_slot = gram_partial_doubles_per_cta(p.mt_out, p.N);
+    int slot_base = 0;
+    for (auto& x : sh) {
+      const int grid = grid_for(x) & ~1;
+      if (x.rows > 0) {
+        for (int wi = 0; wi < 5; ++wi)
+          p.map0[wi] = sp.sp[0].src == SX ? x.mapX[0][wi] : x.mapQ[0][wi];
+        for (int wi = 0; wi < 2; ++wi)
+          p.map1[wi] = sp.sp[1].src == SX ? x.mapX[0][3 + wi] : x.mapQ[0][3 + wi];
+        p.n_rows = x.rows;
+        p.total_stages = (x.rows + 31) / 32;
+        p.partial = c->partial.d() + per_slot * slot_base;
+        p.dstA = x.Q + (size_t)fz.dstA * x.ldq;
+        p.lddA = x.ldq;
+        p.dstB = x.Q + (size_t)fz.dstB * x.ldq;
+        p.lddB = x.ldq;
+        const int nout = (fz.a ? 1 : 0) + (fz.b ? 1 : 0);
+        const double bytes = 8.0 * x.rows * (sp.sp[0].ncols + sp.sp[1].ncols) + 8.0 * x.rows * s * nout;
+        const double flops = 2.0 * x.rows * (double)M * sp.N + 2.0 * x.rows * (double)fz.kp * s * nout;
+        Prof pr(c, "fused_update_gram", bytes, flops);
+        CUDA_OK(k12_launch(p, grid, c->stream, &c->launches));
+        slot_base += grid;
+      } else {
+        CUDA_OK(cudaMemsetAsync(c->partial.d() + per_slot * slot_base, 0,
+                                per_slot * sizeof(double), c->stream));
+        slot_base += 1;
+      }
+    }
+    TileParams rp;
+    memset(&rp, 0, sizeof rp);
+    rp.partial = c->partial.d();
+    rp.mt_out = p.mt_out;
+    rp.N = p.N;
+    rp.units_span[0] = p.U0;
+    rp.lcols[0] = lc[0];
+    rp.lcols[1] = lc[1];
+    rp.status = status;
+    {
+      Prof pr(c, "gram_reduce", (double)slot_base * per_slot * 8.0, 0.0);
+      CUDA_OK(gram_reduce_launch(rp, slot_base, c->G.d(), c->stream, &c->launches));
+    }
+    if (use_nccl && do_allreduce) {
+      Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
+      NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
+                               c->stream));
+    }
+    if (count_sync) record(label, (long)M * p.N);
+    return M;
+  }
+
   // Returns M (rows of the compact Gram written to c->G, ld = M).
   int gram(const GramSpec& sp, const char* label, bool count_sync = true,
            bool do_allreduce = true, const Fuse* fz = nullptr) {
@@ -469,10 +558,14 @@ class Runner {
     p.status = status;
     p.dbg = tile_dbg;
     if (tile_prof) {
-      c->metrics.ensure((size_t)256 * 16 * sizeof(unsigned long long) + 64);
+      c->metrics.ensure((size_t)512 * 16 * sizeof(unsigned long long) + 64);
       p.phase = reinterpret_cast<unsigned long long*>(c->metrics.p);
     }
     const bool upd = fz != nullptr;
+    if (upd && !no_k12c) {
+      const int M = gram_split(sp, label, count_sync, do_allreduce, *fz, units, lc);
+      if (M >= 0) return M;
+    }
     if (upd) {
       if (!tile_fused_supported((int)s, fz->kp, p.mt_out) || sp.N > 8)
         fail(BGS_E_INTERNAL, "gram: fused update not supported for this shape");
@@ -949,7 +1042,7 @@ class Runner {
 
   void dump_phase_profile() {
     if (!tile_prof) return;
-    std::vector<unsigned long long> h(256 * 16);
+    std::vector<unsigned long long> h(512 * 16);
     cudaMemcpy(h.data(), c->metrics.p, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     double tot[16] = {0};
     for (int b = 0; b < 256; ++b)
@@ -961,12 +1054,23 @@ class Runner {
             "flush %.0f | total %.0f\n",
             tot[9], tot[0] / st, tot[1] / st, tot[2] / st, tot[3] / st, tot[4] / st, tot[6] / st,
             tot[7] / st, tot[10] / st, tot[8] / st, tot[5] / st);
+    // K12c: [cta][group][full-wait, update, exchange, epilogue, gram, total, stages]
+    double kt[8] = {0};
+    for (int b = 0; b < 256; ++b)
+      for (int g = 0; g < 2; ++g)
+        for (int i = 0; i < 7; ++i) kt[i] += (double)h[256 * 16 + b * 16 + 8 * g + i];
+    if (kt[6] > 0)
+      fprintf(stderr,
+              "[k12c phases] group-stages %.0f | cycles per group-stage: full-wait %.0f update %.0f "
+              "exchange %.0f epilogue %.0f gram %.0f | total %.0f\n",
+              kt[6], kt[0] / kt[6], kt[1] / kt[6], kt[2] / kt[6], kt[3] / kt[6], kt[4] / kt[6],
+              kt[5] / kt[6]);
   }
 
   void run() {
     if (tile_prof) {
-      c->metrics.ensure((size_t)256 * 16 * sizeof(unsigned long long) + 64);
-      CUDA_OK(cudaMemsetAsync(c->metrics.p, 0, 256 * 16 * sizeof(unsigned long long), c->stream));
+      c->metrics.ensure((size_t)512 * 16 * sizeof(unsigned long long) + 64);
+      CUDA_OK(cudaMemsetAsync(c->metrics.p, 0, 512 * 16 * sizeof(unsigned long long), c->stream));
     }
     setup();
     switch (variant) {
