@@ -313,12 +313,12 @@ class Context:
 
     def read_profile(self) -> Dict[str, Dict[str, float]]:
         """Per kernel class: launches, device ms, algorithmic bytes / flops (resets)."""
-        arr = (_KStat * 64)()
+        arr = (_KStat * 256)()
         cnt = ctypes.c_int()
-        _lib.bgs_profile_read(self._h, arr, 64, ctypes.byref(cnt))
+        _lib.bgs_profile_read(self._h, arr, 256, ctypes.byref(cnt))
         return {arr[i].name.decode(): dict(launches=int(arr[i].launches), ms=arr[i].ms,
                                            alg_bytes=arr[i].alg_bytes, alg_flops=arr[i].alg_flops)
-                for i in range(min(cnt.value, 64))}
+                for i in range(min(cnt.value, 256))}
 
     def close(self) -> None:
         if self._h:

@@ -1,30 +1,42 @@
-// k12.cu — K12c: the block update of step k fused in front of the Gram of step k+1,
-// split over a CTA pair (thread-block cluster of two) with ping-pong consumer groups.
+// k12.cu — K12c: the block update of step k fused in front of the Gram of step k+1, on
+// ping-pong consumer warpgroups, optionally split over a CTA pair (cluster of two).
 //
 // Same algebra and call sites as gram.cu's K12 (onesync_impl bcgs.cpp:329-331, 346-359;
 // pipi_impl bcgs.cpp:196-214):
 //   A = (srcA - Qp CA) TA^{-1},  B = (srcB - Qp CB - A S2) TB^{-1},  G = [tile]^T [span 1]
-// Why a pair: late in a sweep one 32-row stage of the tile is 400+ columns (100+ KB), so
-// a single SM holds two stages and computes one while the other loads — the update, its
-// cross-warp reduction, the epilogue and the Gram then run back to back with nothing to
-// hide their latencies.  Splitting the prefix columns over two SMs halves the stage, so
-// each SM keeps 4 stages: two being computed by two consumer groups (4 warps each,
-// alternate stages, one warp per scheduler each) and two in flight.
 //
-//   rank r of the pair loads: its own span-0 units (the prefix half it contracts), the
-//   A-block units (rank 0 only; rank 1 owns them), and all of span 1 (the B block and
-//   the right-hand columns).  Update: warp w of a group owns rows 8w..8w+7 of the stage
-//   and runs all of this rank's k-steps (coefficients in registers as DMMA B fragments),
-//   giving a partial D (8 rows x [CA | CB]) per warp.  The partial goes to the same warp
-//   of the peer through distributed shared memory (st.async + mbarrier complete_tx);
-//   both ranks form D0 + D1 (same operands, same order -> identical bits), run the
-//   epilogue in registers (quad shuffles, explicit inverses), write A / B back into their
-//   stage, and then contract their own output tiles against span 1.
+// Work unit: a stage of RS = 32 R rows (R = 1, 2, 4 chunks of 32 rows; every chunk has the
+// stage layout of gram.cu with H = 2: 256-byte column runs, SWIZZLE_128B lines).  Each
+// stage costs a roughly fixed latency (update -> reduction -> [exchange] -> epilogue ->
+// Gram with two group barriers), so the plan takes the tallest stage that still leaves
+// >= 3 stages in shared memory: R = 4 for narrow tiles early in a sweep, R = 1 late.
 //
-// Output tiles: rank 0 = own span-0 units + the span-1 left units, rank 1 = its own
-// span-0 units (which include the A block).  Partials: one slot per (cluster, group),
-// every global tile written by exactly one rank -> gram_reduce sums 2 x clusters slots.
+// Warp roles (384 threads, setmaxnreg): warps 0-3 and 4-7 are two consumer groups that take
+// alternate stages (one warp per scheduler each, so one group's latency-bound phases hide
+// behind the other group's DMMAs); warp 8 lane 0 streams stages with TMA; warps 9-11 idle.
+//
+// Cluster width C (runtime):
+//   C = 1: one CTA holds the whole tile (all span-0 units + span 1).
+//   C = 2: late in a sweep one 32-row chunk of the tile is 400+ columns (100+ KB), so the
+//     prefix columns are split over a CTA pair.  Rank r loads its own span-0 units, the
+//     A-block units (rank 0 only; rank 1 owns them) and all of span 1 (B block and right
+//     columns).  Each rank contracts its own k-steps; the partial update of every row is
+//     exchanged through distributed shared memory (st.async + mbarrier complete_tx) and
+//     both ranks form D_0 + D_1 (same operands -> identical bits).
+//
+// Per stage and group:
+//   update   warp w contracts quad (w mod R) (32 rows = 4 m-tiles, one LDS.128 pair per
+//            k-step gives a lane its 4 rows) over k-steps j = w/R + (4/R) t; partials go
+//            through shared memory and the epilogue warp sums the 4/R of them in order.
+//   epilogue on the tensor core: [A | B] = [srcA - DA | srcB - DB] M, M = [[TA^-1,
+//            -TA^-1 W], [0, TB^-1]], W = S2 TB^-1 (2 DMMAs per 8 rows).
+//   Gram     this rank's output tiles (warp w: tiles w + 4jj) against span 1, DMMA.8x8x4,
+//            folded into double-double (hi, lo) after every stage.
+// Output tiles: rank 0 = own span-0 units + the span-1 left units, rank 1 = its own span-0
+// units.  The two groups' double-doubles are combined in the CTA at the end; one partial
+// slot per cluster (every tile written by exactly one rank) -> gram_reduce.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -42,43 +54,48 @@ constexpr int kThreads = 32 * (kConsWarps + 4);
 // setmaxnreg: the producer warpgroup gives registers to the two consumer warpgroups
 // (4 x 32 x (2 x 232 + 40) = 64512 <= 65536)
 constexpr int kProdRegs = 40, kConsRegs = 232;
-constexpr int RS = 32;                    // rows per stage (H = 2: 256-byte column runs)
-constexpr int kUnitBytes = 8 * RS * 8;    // one 8-column unit of a stage
-constexpr int kXchgBytes = kGroups * 2 * kGroupWarps * 32 * 16;  // [group][parity][warp][lane]
+constexpr int kChunkRows = 32;
+constexpr int kUnitChunkBytes = 8 * kChunkRows * 8;  // one 8-column unit of one 32-row chunk
 constexpr int kRedBytes = kGroups * kGroupWarps * 4 * 32 * 16;  // [group][warp][m-tile][lane]
-constexpr int kStaticSmem = 6 * 16 * 8;   // the epilogue factor arrays below
-constexpr int kSmemOptin = 232448;        // per-block opt-in maximum (227 KB)
+__host__ __device__ constexpr int xchg_bytes(int R) { return kGroups * 2 * R * kGroupWarps * 32 * 16; }
+constexpr int kStaticSmem = 2048;  // epilogue factor arrays (ptxas reports 2048 B static)
+constexpr int kSmemOptin = 232448;  // per-block opt-in maximum (227 KB)
 constexpr int kMaxStages = 8;
 
 }  // namespace
 
-size_t k12_smem_bytes(int stages, int slot_units) {
-  return 1024 + (size_t)stages * slot_units * kUnitBytes + kRedBytes + kXchgBytes +
-         (size_t)(2 * stages + 4) * sizeof(uint64_t);
+size_t k12_smem_bytes(int stages, int slot_units, int R, int C) {
+  return 1024 + (size_t)stages * slot_units * R * kUnitChunkBytes + kRedBytes +
+         (C == 2 ? xchg_bytes(R) : 0) + (size_t)(2 * stages + 4) * sizeof(uint64_t);
 }
 
-template <int KW, int MTW>
+template <int KW, int MTW, int R>
 __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant__ SplitParams p) {
   if (p.status && status_bad(p.status)) return;  // both ranks read the same word
+  constexpr int KS = 4 / R;                     // k-split factor of the update
+  constexpr int RS = kChunkRows * R;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const bool pair = p.cluster == 2;
   const int S = p.stages;
-  const int slot_bytes = p.slot_units * kUnitBytes;
+  const int chunk_bytes = p.slot_units * kUnitChunkBytes;
+  const int slot_bytes = R * chunk_bytes;
   unsigned char* redbuf = smem + (size_t)S * slot_bytes;  // [group][warp][m-tile][lane]
-  unsigned char* xbuf = redbuf + kRedBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + kXchgBytes);
+  unsigned char* xbuf = redbuf + kRedBytes;               // [group][parity][chunk][warp][lane]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + (pair ? xchg_bytes(R) : 0));
   uint64_t* empty = full + S;
   uint64_t* xfull = empty + S;  // [group][parity]
-  __shared__ double ep_t[2][16], ep_s2[16], ep_ai[16], ep_bi[16], ep_w[16];
+  __shared__ double ep_t[2][16], ep_s2[16], ep_ai[16], ep_bi[16], ep_w[16], ep_m[64];
 
-  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const uint32_t rank = pair ? cluster_ctarank() : 0u, peer = rank ^ 1u;
   const int own_u0 = p.own_u0[rank], own_n = p.own_n[rank];
   const int ext_u0 = p.ext_u0[rank], ext_n = p.ext_n[rank];
   const int nloc = own_n + ext_n + p.U1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long T = p.total_stages;
-  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int cl = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ncl = pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const long st0 = (long)cl * T / ncl;
   const int nst = (int)((long)(cl + 1) * T / ncl - st0);
   const int s = p.s;
@@ -119,7 +136,25 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     ep_w[m + 4 * j] = acc;
   }
   __syncthreads();
-  cluster_sync_all();  // the peer's mbarriers exist before any st.async can reach them
+  // M[l][j] (row-major 8 x 8): out = z M with z = [srcA - DA, srcB - DB]
+  if (threadIdx.x < 64) {
+    const int l = threadIdx.x >> 3, j = threadIdx.x & 7;
+    double v = 0.0;
+    if (l < 4 && j < 4) {
+      v = p.upd_a ? ep_ai[l + 4 * j] : 0.0;
+    } else if (l < 4) {  // -(TA^-1 W)[l][j-4]
+      if (p.upd_a && p.upd_b) {
+        double acc = 0.0;
+        for (int m = 0; m < 4; ++m) acc += ep_ai[l + 4 * m] * ep_w[m + 4 * (j - 4)];
+        v = -acc;
+      }
+    } else if (j >= 4) {
+      v = p.upd_b ? ep_bi[(l - 4) + 4 * (j - 4)] : 0.0;
+    }
+    ep_m[l * 8 + j] = v;
+  }
+  __syncthreads();
+  if (pair) cluster_sync_all();  // the peer's mbarriers exist before any st.async reaches them
 
   if (warp >= kProdWarp) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
@@ -131,32 +166,35 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     if (warp == kProdWarp && lane == 0) {
       for (int i = 0; i < 5; ++i) prefetch_tmap(&p.map0[i]);
       for (int i = 0; i < 2; ++i) prefetch_tmap(&p.map1[i]);
-      const uint32_t bytes = (uint32_t)nloc * kUnitBytes;
+      const uint32_t bytes = (uint32_t)(nloc * R * kUnitChunkBytes);
       for (int it = 0; it < nst; ++it) {
         const int slot = it % S;
         if (it >= S) mbar_wait(&empty[slot], ((it / S) - 1) & 1);
         mbar_arrive_expect_tx(&full[slot], bytes);
-        unsigned char* dst = smem + (size_t)slot * slot_bytes;
-        const int rb = (int)((st0 + it) * 2);  // first 16-row block of the stage
-        int u = 0;
-        for (int seg = 0; seg < 3; ++seg) {  // own span-0 units, extra units, span 1
-          int left = seg == 0 ? own_n : seg == 1 ? ext_n : p.U1;
-          int c = seg == 0 ? p.col0[0] + 8 * own_u0 : seg == 1 ? p.col0[0] + 8 * ext_u0 : p.col0[1];
-          while (left > 0) {
-            int wi;
-            const CUtensorMap* mp;
-            if (seg < 2) {
-              wi = left >= 16 ? 0 : left >= 8 ? 1 : left >= 4 ? 2 : left >= 2 ? 3 : 4;
-              mp = &p.map0[wi];
-            } else {
-              wi = left >= 2 ? 3 : 4;
-              mp = &p.map1[wi - 3];
+#pragma unroll 1
+        for (int ch = 0; ch < R; ++ch) {
+          unsigned char* dst = smem + (size_t)slot * slot_bytes + (size_t)ch * chunk_bytes;
+          const int rb = (int)((st0 + it) * 2 * R + 2 * ch);  // first 16-row block of the chunk
+          int u = 0;
+          for (int seg = 0; seg < 3; ++seg) {  // own span-0 units, extra units, span 1
+            int left = seg == 0 ? own_n : seg == 1 ? ext_n : p.U1;
+            int c = seg == 0 ? p.col0[0] + 8 * own_u0 : seg == 1 ? p.col0[0] + 8 * ext_u0 : p.col0[1];
+            while (left > 0) {
+              int wi;
+              const CUtensorMap* mp;
+              if (seg < 2) {
+                wi = left >= 16 ? 0 : left >= 8 ? 1 : left >= 4 ? 2 : left >= 2 ? 3 : 4;
+                mp = &p.map0[wi];
+              } else {
+                wi = left >= 2 ? 3 : 4;
+                mp = &p.map1[wi - 3];
+              }
+              const int wu = 16 >> wi;
+              tma_load_3d(dst + (size_t)u * kUnitChunkBytes, mp, &full[slot], 0, rb, c);
+              u += wu;
+              c += 8 * wu;
+              left -= wu;
             }
-            const int wu = 16 >> wi;
-            tma_load_3d(dst + (size_t)u * kUnitBytes, mp, &full[slot], 0, rb, c);
-            u += wu;
-            c += 8 * wu;
-            left -= wu;
           }
         }
       }
@@ -166,18 +204,21 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     // ---------------- consumers: group g takes stages g, g+2, g+4, ... ----------------
     const int g = warp / kGroupWarps, w = warp % kGroupWarps;
     const int gtid = threadIdx.x - 32 * kGroupWarps * g;
-    const int ii = lane >> 2, kk = lane & 3, odd = ii & 1;
+    const int ii = lane >> 2, kk = lane & 3;
     const int gbar = 1 + g;
-    // This rank's k-steps are prefix columns [8 own_u0, pc1) (local columns from 0); warp w
-    // takes k-steps j = w + 4t.  Lane (ii, kk) holds C[4j + kk][n = ii] of [CA | CB]
-    // (CA in n = 0..3, CB in n = 4..7, zero padded) as the DMMA B fragment.
+    // Update: this rank's k-steps are prefix columns [8 own_u0, pc1) (local columns from
+    // 0); warp w contracts quad qd = w mod R over k-steps j = kpart + KS t.  Lane (ii, kk)
+    // holds C[4j + kk][n = ii] of [CA | CB] (CA in n = 0..3, CB in n = 4..7, zero padded)
+    // as the DMMA B fragment.
+    const int qd = w % R, kpart = w / R;
     const int pc1 = min(8 * (own_u0 + own_n), p.kp);
     const int kcols = max(0, pc1 - 8 * own_u0);
     const int ksteps = kcols / 4;  // whole k-steps (k12_plan)
+    const int jlast = max(ksteps - 1, 0);
     double bco[KW];
 #pragma unroll
     for (int t = 0; t < KW; ++t) {
-      const int lc = 4 * (w + kGroupWarps * t) + kk, c = 8 * own_u0 + lc;
+      const int lc = 4 * (kpart + KS * t) + kk, c = 8 * own_u0 + lc;
       double v = 0.0;
       if (lc < kcols) {
         if (ii < 4) {
@@ -188,17 +229,18 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       }
       bco[t] = v;
     }
-    // Update A fragments: m-tile q is rows {4i + q}, so lane (ii, kk) needs rows
-    // 4ii..4ii+3 of tile column 4j + kk: two LDS.128 (frag4 with h = ii/4, kk' = ii%4).
-    // Column 4j + kk sits on line 8j + 2kk + ii/4, i.e. at 1024 j past k-step 0.
+    // Update A fragments: m-tile q, row index i is chunk row 4 f(i) + q with
+    // f(i) = (i >> 1) + 4 (i & 1), so lane (i, kk) reads rows 4f..4f+3 of tile column
+    // 4j + kk with two LDS.128 (line 8j + 2kk + (i & 1), 1024 j past k-step 0).  The two
+    // i of a quarter-warp sit in different 16-row halves -> chunk sets {2a ^ 2kk} and
+    // {2a ^ (2kk + 1)} are disjoint: conflict-free with no lane swap.
     uint32_t uoff0, uoff1;
     {
-      const int line = 2 * kk + (ii >> 2);
-      const int o = (ii & 3) & 1;
-      uoff0 = (uint32_t)(line * 128 + ((((ii & 3) * 2 + o) ^ (line & 7)) << 4));
-      uoff1 = (uint32_t)(line * 128 + ((((ii & 3) * 2 + 1 - o) ^ (line & 7)) << 4));
+      const int line = 2 * kk + (ii & 1);
+      const int rc = 2 * (ii >> 1);  // chunk of rows 4f, 4f + 1 inside the 16-row block
+      uoff0 = (uint32_t)(line * 128 + ((rc ^ (line & 7)) << 4));
+      uoff1 = (uint32_t)(line * 128 + (((rc + 1) ^ (line & 7)) << 4));
     }
-    const bool uswap = ((ii & 3) & 1) != 0;
     // local columns of the A block, the B block (= span-1 column 0) and the right operand
     const bool a_own = p.kp >= 8 * own_u0 && p.kp < 8 * (own_u0 + own_n);
     const int colA = a_own ? p.kp - 8 * own_u0 : 8 * own_n + p.kp - 8 * ext_u0;
@@ -208,10 +250,22 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     const int bcol = colB + (bval ? rc : 0);
     // output tiles of this rank: own units, then (rank 0) the span-1 left units
     const int mt_loc = own_n + (rank == 0 ? p.s1_left : 0);
-    // epilogue row of this lane: warp w handles rows 8w..8w+7 (coalesced stores)
-    const int qsel = lane >> 3, isel = 2 * w + ((lane >> 2) & 1);
-    const int erow = 4 * isel + qsel;
+    // Epilogue: warp w handles rows 8w + m (m = lane / 4) of every chunk (coalesced
+    // stores); in the update that row is m-tile q = m & 3, index i with
+    // f(i) = 2w + (m >> 2), of the chunk's quad.
+    const int erow = 8 * w + ii;
+    const int qsel = ii & 3, vsel = 2 * w + (ii >> 2), isel = 2 * (vsel & 3) + (vsel >> 2);
     const int quad = lane & ~3;
+    // epilogue matrix M as DMMA B fragments: lane (i, kk) holds M[kk][i] and M[4 + kk][i]
+    const double mb0 = ep_m[kk * 8 + ii], mb1 = ep_m[(4 + kk) * 8 + ii];
+    int acol[MTW];  // tile column of this lane's Gram fragment, per output tile
+#pragma unroll
+    for (int jj = 0; jj < MTW; ++jj) {
+      int t = w + kGroupWarps * jj;
+      if (t >= mt_loc) t = w < mt_loc ? w : 0;
+      const int lu = t < own_n ? t : t + ext_n;
+      acol[jj] = 8 * lu + ii;
+    }
 
     double hi[MTW][2], lo[MTW][2];
 #pragma unroll
@@ -220,9 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       for (int e = 0; e < 2; ++e) hi[j][e] = lo[j][e] = 0.0;
 
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t red_w = smem_u32(redbuf) + (uint32_t)(((g * kGroupWarps + w) * 4 * 32 + lane) * 16);
-    const uint32_t red_r = smem_u32(redbuf) +
-                           (uint32_t)(((g * kGroupWarps * 4 + qsel) * 32 + 4 * isel + kk) * 16);
+    const uint32_t red_g = smem_u32(redbuf) + (uint32_t)(g * kGroupWarps * 4 * 32 * 16);
+    const uint32_t red_w = red_g + (uint32_t)((w * 4 * 32 + lane) * 16);
+    const uint32_t red_r = red_g + (uint32_t)((qsel * 32 + 4 * isel + kk) * 16);
     const uint32_t xb_local = smem_u32(xbuf);
     const uint32_t xfull_local = smem_u32(xfull);
     const bool prof = p.phase && gtid == 0;
@@ -242,104 +296,113 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       if (vrows < RS) {
         // rows past the shard end inside its last 16-row block are not TMA zero-filled
         const int ncol = nloc * 8, nr = RS - vrows;
-        for (int e = gtid; e < ncol * nr; e += 32 * kGroupWarps)
-          sts64(base + elem_off<2>(e / nr, vrows + e % nr), 0.0);
+        for (int e = gtid; e < ncol * nr; e += 32 * kGroupWarps) {
+          const int r = vrows + e % nr;
+          sts64(base + (uint32_t)((r >> 5) * chunk_bytes) + elem_off<2>(e / nr, r & 31), 0.0);
+        }
         bar_named(gbar, 32 * kGroupWarps);
       }
 
-      // ---- update partial: all 32 rows (4 m-tiles = 4 DMMA chains), k-steps w + 4t ----
-      double d[4][2];
+      // ---- update partial: quad qd (4 m-tiles = 4 DMMA chains), k-steps kpart + KS t ----
+      // Branch-free so ptxas can hoist the loads of later k-steps: k-steps past this
+      // rank's range have zero coefficients and read the last valid k-step (finite data).
+      {
+        double d[4][2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) d[q][0] = d[q][1] = 0.0;
+        for (int q = 0; q < 4; ++q) d[q][0] = d[q][1] = 0.0;
+        const uint32_t cb = base + (uint32_t)(qd * chunk_bytes);
 #pragma unroll
-      for (int t = 0; t < KW; ++t) {
-        const int jk = w + kGroupWarps * t;
-        if (jk < ksteps) {
-          const uint32_t a = base + 1024u * (uint32_t)jk;
+        for (int t = 0; t < KW; ++t) {
+          const int jk = min(kpart + KS * t, jlast);
+          const uint32_t a = cb + 1024u * (uint32_t)jk;
           const double2 x0 = lds128(a + uoff0), x1 = lds128(a + uoff1);
-          const double v0 = uswap ? x1.x : x0.x, v1 = uswap ? x1.y : x0.y;
-          const double v2 = uswap ? x0.x : x1.x, v3 = uswap ? x0.y : x1.y;
-          dmma(d[0][0], d[0][1], v0, bco[t]);
-          dmma(d[1][0], d[1][1], v1, bco[t]);
-          dmma(d[2][0], d[2][1], v2, bco[t]);
-          dmma(d[3][0], d[3][1], v3, bco[t]);
+          dmma(d[0][0], d[0][1], x0.x, bco[t]);
+          dmma(d[1][0], d[1][1], x0.y, bco[t]);
+          dmma(d[2][0], d[2][1], x1.x, bco[t]);
+          dmma(d[3][0], d[3][1], x1.y, bco[t]);
         }
-      }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) sts128(red_w + (uint32_t)(q * 32 * 16), d[q][0], d[q][1]);
+        for (int q = 0; q < 4; ++q) sts128(red_w + (uint32_t)(q * 32 * 16), d[q][0], d[q][1]);
+      }
       bar_named(gbar, 32 * kGroupWarps);
       if (prof) { const unsigned long long t = clock64(); ph[1] += t - t1; t1 = t; }
 
-      // ---- sum the 4 warp partials of this lane's row, exchange with the peer (DSMEM) ----
-      double D0 = 0.0, D1 = 0.0;
+      // ---- per chunk: sum the KS warp partials of this lane's row (fixed order) ----
+      double D0[R], D1[R];
 #pragma unroll
-      for (int ws = 0; ws < kGroupWarps; ++ws) {
-        const double2 v = lds128(red_r + (uint32_t)(ws * 4 * 32 * 16));
-        D0 += v.x;
-        D1 += v.y;
+      for (int ch = 0; ch < R; ++ch) {
+        D0[ch] = D1[ch] = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < KS; ++k2) {
+          const int ws = ch + R * k2;  // warp that contracted quad ch, k-part k2
+          const double2 v = lds128(red_r + (uint32_t)(ws * 4 * 32 * 16));
+          D0[ch] += v.x;
+          D1[ch] += v.y;
+        }
       }
-      const int xb = g * 2 + (j & 1);
-      const uint32_t mine = xb_local + (uint32_t)(((xb * kGroupWarps + w) * 32 + lane) * 16);
-      st_async_v2f64(mapa_shared(mine, peer), D0, D1,
-                     mapa_shared(xfull_local + (uint32_t)(xb * 8), peer));
-      if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], kGroupWarps * 32 * 16);
-      mbar_wait_cluster(&xfull[xb], (j >> 1) & 1);
-      {
-        const double2 o = lds128(mine);
-        D0 += o.x;  // IEEE addition commutes: both ranks hold (rank 0) + (rank 1)
-        D1 += o.y;
+      if (pair) {
+        // ---- exchange with the same warp of the peer rank (DSMEM) ----
+        const int xb = g * 2 + (j & 1);
+        const uint32_t rbar = mapa_shared(xfull_local + (uint32_t)(xb * 8), peer);
+#pragma unroll
+        for (int ch = 0; ch < R; ++ch) {
+          const uint32_t mine =
+              xb_local + (uint32_t)((((xb * R + ch) * kGroupWarps + w) * 32 + lane) * 16);
+          st_async_v2f64(mapa_shared(mine, peer), D0[ch], D1[ch], rbar);
+        }
+        if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], R * kGroupWarps * 32 * 16);
+        mbar_wait(&xfull[xb], (j >> 1) & 1);  // data and completion are both CTA-local
+#pragma unroll
+        for (int ch = 0; ch < R; ++ch) {
+          const uint32_t mine =
+              xb_local + (uint32_t)((((xb * R + ch) * kGroupWarps + w) * 32 + lane) * 16);
+          const double2 o = lds128(mine);
+          D0[ch] += o.x;  // IEEE addition commutes: both ranks hold (rank 0) + (rank 1)
+          D1[ch] += o.y;
+        }
       }
       if (prof) { const unsigned long long t = clock64(); ph[2] += t - t1; t1 = t; }
 
-      // ---- epilogue: every lane of a quad forms the row's A and B; lane kk stores col kk ----
-      double Dv[8];
+      // ---- epilogue on the tensor core: [A | B] = [srcA - DA | srcB - DB] M ----
+      // A operand lane (i, kk): z[row][kk] and z[row][4 + kk]; D[row][c] sits in lane
+      // (i, c / 2), element c & 1.
 #pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        Dv[2 * l] = __shfl_sync(0xffffffffu, D0, quad | l);
-        Dv[2 * l + 1] = __shfl_sync(0xffffffffu, D1, quad | l);
-      }
-      double A[4] = {0.0, 0.0, 0.0, 0.0}, B[4] = {0.0, 0.0, 0.0, 0.0};
-      if (p.upd_a) {
-        double x[4];
+      for (int ch = 0; ch < R; ++ch) {
+        const uint32_t cb = base + (uint32_t)(ch * chunk_bytes);
+        const int sl = quad | (kk >> 1);
+        const double t0 = __shfl_sync(0xffffffffu, D0[ch], sl), t1 = __shfl_sync(0xffffffffu, D1[ch], sl);
+        const double u0 = __shfl_sync(0xffffffffu, D0[ch], sl | 2);
+        const double u1 = __shfl_sync(0xffffffffu, D1[ch], sl | 2);
+        const bool cv = kk < s;
+        const double sa = (p.upd_a && cv) ? lds64(cb + elem_off<2>(colA + kk, erow)) : 0.0;
+        const double sb = (p.upd_b && cv) ? lds64(cb + elem_off<2>(colB + kk, erow)) : 0.0;
+        const double za = (p.upd_a && cv) ? sa - ((kk & 1) ? t1 : t0) : 0.0;
+        const double zb = (p.upd_b && cv) ? sb - ((kk & 1) ? u1 : u0) : 0.0;
+        double o0 = 0.0, o1 = 0.0;
+        dmma(o0, o1, za, mb0);
+        dmma(o0, o1, zb, mb1);
+        // lane (i, kk) now holds output columns 2kk, 2kk + 1: A for kk < 2, B for kk >= 2
+        const bool isA = kk < 2;
+        const int c0 = isA ? 2 * kk : 2 * kk - 4;
+        const bool on = isA ? p.upd_a : p.upd_b;
+        const int lcol = isA ? colA : colB;
+        const int crow = kChunkRows * ch + erow;
+        const bool live = crow < vrows;
+        const long grow = row0 + crow;
+        double* gdst = isA ? p.dstA : p.dstB;
+        const long gld = isA ? p.lddA : p.lddB;
+        // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
+        // shared: A only where its rows are output tiles (the rank owning the A units)
+        const bool gstore = live && (!pair || (isA ? rank == 0 : rank == 1));
+        const bool sstore = isA ? (!pair || rank == 1) : true;
 #pragma unroll
-        for (int l = 0; l < 4; ++l)
-          x[l] = l < s ? lds64(base + elem_off<2>(colA + l, erow)) - Dv[l] : 0.0;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          double a = 0.0;
-#pragma unroll
-          for (int l = 0; l <= jj; ++l) a += x[l] * ep_ai[l + 4 * jj];
-          A[jj] = a;
-        }
-      }
-      if (p.upd_b) {
-        double y[4];
-#pragma unroll
-        for (int l = 0; l < 4; ++l)
-          y[l] = l < s ? lds64(base + elem_off<2>(colB + l, erow)) - Dv[4 + l] : 0.0;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          double b = 0.0;
-#pragma unroll
-          for (int l = 0; l < 4; ++l) {
-            if (l <= jj) b += y[l] * ep_bi[l + 4 * jj];
-            b -= A[l] * ep_w[l + 4 * jj];
+        for (int e = 0; e < 2; ++e) {
+          const int c = c0 + e;
+          if (on && c < s) {
+            const double v = e ? o1 : o0;
+            if (sstore) sts64(cb + elem_off<2>(lcol + c, erow), v);
+            if (gstore) gdst[grow + (size_t)c * gld] = v;
           }
-          B[jj] = b;
-        }
-      }
-      if (kk < s) {
-        const double av = kk == 0 ? A[0] : kk == 1 ? A[1] : kk == 2 ? A[2] : A[3];
-        const double bv = kk == 0 ? B[0] : kk == 1 ? B[1] : kk == 2 ? B[2] : B[3];
-        const bool live = erow < vrows;
-        const long grow = row0 + erow;
-        if (p.upd_a) {
-          if (rank == 1) sts64(base + elem_off<2>(colA + kk, erow), av);  // rank 1 owns A's rows
-          if (rank == 0 && live) p.dstA[grow + (size_t)kk * p.lddA] = av;
-        }
-        if (p.upd_b) {
-          sts64(base + elem_off<2>(colB + kk, erow), bv);
-          if (rank == 1 && live) p.dstB[grow + (size_t)kk * p.lddB] = bv;
         }
       }
       bar_named(gbar, 32 * kGroupWarps);
@@ -349,25 +412,35 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       double acc[MTW][2];
 #pragma unroll
       for (int jj = 0; jj < MTW; ++jj) acc[jj][0] = acc[jj][1] = 0.0;
+      // k-index kk of pass u covers chunk rows 16 (kk & 1) + 8 (kk >> 1) + 4u + {0..3}: for
+      // the two tile columns of a quarter-warp the chunk sets are S and S ^ 2 with
+      // S = {0, 1, 4, 5} (u = 0) or {2, 3, 6, 7} (u = 1) -> conflict-free, no swap.
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double b[4];
-        frag4<2>(base, bcol, h, kk, odd, b);
-        if (!bval) b[0] = b[1] = b[2] = b[3] = 0.0;
+      for (int ch = 0; ch < R; ++ch) {
+        const uint32_t cb = base + (uint32_t)(ch * chunk_bytes);
 #pragma unroll
-        for (int jp = 0; jp < MTW; jp += 2) {
-          const int t0i = w + kGroupWarps * jp, t1i = t0i + kGroupWarps;
-          if (t0i < mt_loc) {
-            const bool two = jp + 1 < MTW && t1i < mt_loc;
-            const int lu0 = t0i < own_n ? t0i : t0i + ext_n;
-            const int lu1 = two ? (t1i < own_n ? t1i : t1i + ext_n) : lu0;
+        for (int u = 0; u < 2; ++u) {
+          const int gh = kk & 1, rcu = 4 * (kk >> 1) + 2 * u;  // half, chunk of the first row pair
+          auto gfrag = [&](int col, double (&v)[4]) {
+            const int line = 2 * col + gh;
+            const uint32_t bl = cb + (uint32_t)(line * 128);
+            const double2 x0 = lds128(bl + (uint32_t)((rcu ^ (line & 7)) << 4));
+            const double2 x1 = lds128(bl + (uint32_t)(((rcu + 1) ^ (line & 7)) << 4));
+            v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
+          };
+          double b[4];
+          gfrag(bcol, b);
+          if (!bval) b[0] = b[1] = b[2] = b[3] = 0.0;
+          // branch-free: tiles past mt_loc re-read a valid tile; dropped at the end
+#pragma unroll
+          for (int jp = 0; jp < MTW; jp += 2) {
             double a0[4], a1[4];
-            frag4<2>(base, 8 * lu0 + ii, h, kk, odd, a0);
-            frag4<2>(base, 8 * lu1 + ii, h, kk, odd, a1);
+            gfrag(acol[jp], a0);
+            if (jp + 1 < MTW) gfrag(acol[jp + 1], a1);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
               dmma(acc[jp][0], acc[jp][1], a0[q4], b[q4]);
-              if (jp + 1 < MTW && two) dmma(acc[jp + 1][0], acc[jp + 1][1], a1[q4], b[q4]);
+              if (jp + 1 < MTW) dmma(acc[jp + 1][0], acc[jp + 1][1], a1[q4], b[q4]);
             }
           }
         }
@@ -392,28 +465,52 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       for (int i = 0; i < 6; ++i) atomicAdd(&dst[i], ph[i]);
       atomicAdd(&dst[6], (unsigned long long)((nst - g + 1) / 2));
     }
-    double2* part = reinterpret_cast<double2*>(p.partial) + (size_t)(cl * 2 + g) * p.mt_out * 64;
+    // ---- combine the two groups' double-doubles in a fixed order, one slot per cluster ----
+    // Both groups are past their last stage after this barrier, so every TMA write has
+    // landed and the stage ring (>= MTW x 4 KB: a tile needs its unit in every slot) is free.
+    bar_named(3, 32 * kConsWarps);
+    const uint32_t park = sbase;
+    if (g == 1) {
 #pragma unroll
-    for (int jj = 0; jj < MTW; ++jj) {
-      const int t = w + kGroupWarps * jj;
-      if (t < mt_loc) {
-        const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
+      for (int jj = 0; jj < MTW; ++jj)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          part[((size_t)tg * 8 + ii) * 8 + 2 * kk + e] = make_double2(hi[jj][e], lo[jj][e]);
+          sts128(park + (uint32_t)((((w * MTW + jj) * 2 + e) * 32 + lane) * 16), hi[jj][e], lo[jj][e]);
+    }
+    bar_named(3, 32 * kConsWarps);
+    if (g == 0) {
+      double2* part = reinterpret_cast<double2*>(p.partial) + (size_t)cl * p.mt_out * 64;
+#pragma unroll
+      for (int jj = 0; jj < MTW; ++jj) {
+        const int t = w + kGroupWarps * jj;
+        if (t < mt_loc) {
+          const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double2 o = lds128(park + (uint32_t)((((w * MTW + jj) * 2 + e) * 32 + lane) * 16));
+            double sm, err;
+            two_sum(hi[jj][e], o.x, sm, err);
+            part[((size_t)tg * 8 + ii) * 8 + 2 * kk + e] = make_double2(sm, err + (lo[jj][e] + o.y));
+          }
+        }
       }
     }
   }
-  cluster_sync_all();  // no CTA leaves while its peer may still address its shared memory
+  if (pair) cluster_sync_all();  // no CTA leaves while its peer may still address its smem
 }
 
 // ------------------------------------------------------------------------------------
 // Host side
 // ------------------------------------------------------------------------------------
 namespace {
-// instances: KW k-steps per warp in {2, 4, ..., 16}, MTW = KW / 2 output tiles per warp
-constexpr int kKwStep = 2, kKwMax = 16;
-int mtw_for(int kw_t) { return (kw_t + 1) / 2; }
+// instances: KW k-steps per warp in {2, 4, ..., 16} for each R; MTW covers the output
+// tiles the plan can give a warp at that KW (C = 1: mt <= KS KW / 2 + 3)
+__host__ __device__ constexpr int mtw_for(int kw, int R) { return ((4 / R) * kw / 2 + 3 + 3) / 4; }
+constexpr int kKwMax = 16;
+
+struct Cand {
+  int C, R;
+};
 }  // namespace
 
 bool k12_plan(SplitParams& p) {
@@ -422,41 +519,71 @@ bool k12_plan(SplitParams& p) {
     if (p.rcol1[j] < 0 || p.rcol1[j] >= 8 * p.U1) return false;
   const int na = p.upd_a ? p.U0 - p.kp / 8 : 0;  // units holding the A block (span-0 tail)
   if (na < 0 || na > p.U0) return false;
-  const int uh = (p.U0 - na + 1) / 2;
-  p.own_u0[0] = 0;       p.own_n[0] = uh;
-  p.ext_u0[0] = p.U0 - na; p.ext_n[0] = na;
-  p.own_u0[1] = uh;      p.own_n[1] = p.U0 - uh;
-  p.ext_u0[1] = 0;       p.ext_n[1] = 0;
   p.s1_left = (p.lcols1 + 7) / 8;
   p.mt_out = p.U0 + p.s1_left;
-  p.slot_units = std::max(uh + na, p.U0 - uh) + p.U1;
-  const int c0 = std::min(8 * uh, p.kp), c1 = std::max(0, p.kp - 8 * uh);
-  if (c0 % 4 || c1 % 4) return false;  // whole k-steps only (always true for s = 4)
-  const int k0 = c0 / 4, k1 = c1 / 4;
-  const int kw = (std::max(k0, k1) + kGroupWarps - 1) / kGroupWarps;
-  const int mt = std::max(uh + p.s1_left, p.U0 - uh);
-  const int mtw = (mt + kGroupWarps - 1) / kGroupWarps;
-  int kw_t = std::max(kKwStep, (kw + kKwStep - 1) / kKwStep * kKwStep);
-  while (mtw_for(kw_t) < mtw) kw_t += kKwStep;
-  if (kw_t > kKwMax) return false;
-  p.kw = kw_t;
-  p.mtw = mtw_for(kw_t);
-  int S = 0;
-  for (int st = kMaxStages; st >= 2; --st)
-    if (k12_smem_bytes(st, p.slot_units) + kStaticSmem + 256 <= (size_t)kSmemOptin) {
-      S = st;
-      break;
+  // C = 1 with the tallest stage that keeps >= 3 stages in shared memory, then the pair
+  const Cand cands[] = {{1, 4}, {1, 2}, {1, 1}, {2, 2}, {2, 1}};
+  // BGS_K12C_PLAN=CR (e.g. 21): only that candidate (experiments)
+  static const int forced = [] {
+    const char* e = getenv("BGS_K12C_PLAN");
+    return e ? atoi(e) : 0;
+  }();
+  for (const Cand& cd : cands) {
+    if (forced && forced != 10 * cd.C + cd.R) continue;
+    SplitParams q = p;
+    q.cluster = cd.C;
+    q.R = cd.R;
+    int k0, k1 = 0, mt0, mt1 = 0;
+    if (cd.C == 1) {
+      q.own_u0[0] = 0; q.own_n[0] = p.U0; q.ext_u0[0] = 0; q.ext_n[0] = 0;
+      q.own_u0[1] = q.own_n[1] = q.ext_u0[1] = q.ext_n[1] = 0;
+      q.slot_units = p.U0 + p.U1;
+      if (p.kp % 4) continue;
+      k0 = p.kp / 4;
+      mt0 = p.U0 + q.s1_left;
+    } else {
+      const int uh = (p.U0 - na + 1) / 2;
+      q.own_u0[0] = 0;         q.own_n[0] = uh;
+      q.ext_u0[0] = p.U0 - na; q.ext_n[0] = na;
+      q.own_u0[1] = uh;        q.own_n[1] = p.U0 - uh;
+      q.ext_u0[1] = 0;         q.ext_n[1] = 0;
+      q.slot_units = std::max(uh + na, p.U0 - uh) + p.U1;
+      const int c0 = std::min(8 * uh, p.kp), c1 = std::max(0, p.kp - 8 * uh);
+      if (c0 % 4 || c1 % 4) continue;  // whole k-steps only (always true for s = 4)
+      k0 = c0 / 4;
+      k1 = c1 / 4;
+      mt0 = uh + q.s1_left;
+      mt1 = p.U0 - uh;
     }
-  if (S < 3) return false;
-  p.stages = S;
-  return true;
+    const int KS = 4 / cd.R;
+    const int kw = (std::max(k0, k1) + KS - 1) / KS;
+    const int mtw = (std::max(mt0, mt1) + kGroupWarps - 1) / kGroupWarps;
+    // (KW = 16 with R = 1 needs MTW = 9 and spills; that shape goes to the pair instead)
+    const int kw_max = cd.R == 1 ? 14 : kKwMax;
+    int kw_t = std::max(2, (kw + 1) / 2 * 2);
+    while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) kw_t += 2;
+    if (kw_t > kw_max) continue;
+    int S = 0;
+    for (int st = kMaxStages; st >= 3; --st)
+      if (k12_smem_bytes(st, q.slot_units, cd.R, cd.C) + kStaticSmem + 256 <= (size_t)kSmemOptin) {
+        S = st;
+        break;
+      }
+    if (!S) continue;
+    q.kw = kw_t;
+    q.mtw = mtw_for(kw_t, cd.R);
+    q.stages = S;
+    p = q;
+    return true;
+  }
+  return false;
 }
 
-template <int KW>
+template <int KW, int R>
 static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
-  constexpr int MTW = (KW + 1) / 2;
-  auto k = k12_kernel<KW, MTW>;
-  const size_t smem = k12_smem_bytes(p.stages, p.slot_units);
+  constexpr int MTW = mtw_for(KW, R);
+  auto k = k12_kernel<KW, MTW, R>;
+  const size_t smem = k12_smem_bytes(p.stages, p.slot_units, R, p.cluster);
   cudaError_t e = ensure_smem(k, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -470,22 +597,34 @@ static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = p.cluster == 2 ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, p);
 }
 
-cudaError_t k12_launch(const SplitParams& p, int grid, cudaStream_t st, int* launches) {
-  if (grid < 2 || (grid & 1)) return cudaErrorInvalidValue;
-  if (launches) *launches += 1;
+template <int R>
+static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
   switch (p.kw) {
-    case 2: return launch_k12<2>(p, grid, st);
-    case 4: return launch_k12<4>(p, grid, st);
-    case 6: return launch_k12<6>(p, grid, st);
-    case 8: return launch_k12<8>(p, grid, st);
-    case 10: return launch_k12<10>(p, grid, st);
-    case 12: return launch_k12<12>(p, grid, st);
-    case 14: return launch_k12<14>(p, grid, st);
-    case 16: return launch_k12<16>(p, grid, st);
+    case 2: return launch_k12<2, R>(p, grid, st);
+    case 4: return launch_k12<4, R>(p, grid, st);
+    case 6: return launch_k12<6, R>(p, grid, st);
+    case 8: return launch_k12<8, R>(p, grid, st);
+    case 10: return launch_k12<10, R>(p, grid, st);
+    case 12: return launch_k12<12, R>(p, grid, st);
+    case 14: return launch_k12<14, R>(p, grid, st);
+    case 16:
+      if (R == 1) return cudaErrorInvalidValue;  // not planned (spills)
+      return launch_k12<16, R == 1 ? 2 : R>(p, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t k12_launch(const SplitParams& p, int grid, cudaStream_t st, int* launches) {
+  if (grid < p.cluster || grid % p.cluster) return cudaErrorInvalidValue;
+  if (launches) *launches += 1;
+  switch (p.R) {
+    case 1: return launch_r<1>(p, grid, st);
+    case 2: return launch_r<2>(p, grid, st);
+    case 4: return launch_r<4>(p, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }

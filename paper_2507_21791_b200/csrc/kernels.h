@@ -62,9 +62,10 @@ int gram_n_tiles(int N);
 size_t gram_partial_doubles_per_cta(int mt_out, int N);
 
 // ---------------- K12c: cluster-split fused update + Gram (k12.cu) ----------------
-// A CTA pair shares each 32-row stage: rank r loads its own span-0 units plus the
-// extra (A-block) units it needs and all of span 1; the partial block update is
-// exchanged through distributed shared memory.  s <= 4, N <= 8.
+// Stages of 32 R rows on ping-pong consumer warpgroups; with cluster = 2 a CTA pair shares
+// each stage: rank r loads its own span-0 units plus the extra (A-block) units it needs and
+// all of span 1, and the partial block update is exchanged through distributed shared
+// memory.  s <= 4, N <= 8.  One (hi, lo) partial slot per cluster.
 struct alignas(64) SplitParams {
   CUtensorMap map0[5];  // span 0, boxes {16, 2, w}, w = 128/64/32/16/8
   CUtensorMap map1[2];  // span 1, w = 16/8
@@ -82,6 +83,8 @@ struct alignas(64) SplitParams {
   long n_rows;
   long total_stages;    // 32-row stages of the shard
   int stages;           // ring depth
+  int cluster;          // CTAs per cluster: 1 (whole tile per CTA) or 2 (split prefix)
+  int R;                // 32-row chunks per stage (1, 2, 4)
   int kw, mtw;          // k-steps / output tiles per warp (planned; selects the instance)
   int upd_a, upd_b, kp, s;
   const double* CA; int ldca; const double* TA;
@@ -96,7 +99,7 @@ struct alignas(64) SplitParams {
 // Plans the rank split for a fused Gram of the given shape; false when K12c does not
 // apply (then the caller uses tile_launch).  Fills own/ext ranges, slot_units, stages.
 bool k12_plan(SplitParams& p);
-size_t k12_smem_bytes(int stages, int slot_units);
+size_t k12_smem_bytes(int stages, int slot_units, int R, int C);
 cudaError_t k12_launch(const SplitParams& p, int grid, cudaStream_t st, int* launches);
 
 // ---------------- K2: block update (update.cu) ----------------

@@ -318,6 +318,7 @@ class Runner {
 
   bool no_fuse = false;
   bool no_k12c = false;
+  bool prof_step = false;  // BGS_PROF_STEP: one profiler class per fused block step
   int tile_dbg = 0;
   bool tile_prof = false;
 
@@ -325,9 +326,11 @@ class Runner {
       : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {
     const char* e = getenv("BGS_NO_FUSE");
     no_fuse = e && *e && *e != '0';
-    // K12c (cluster-split fused kernel) is opt-in until it beats the single-CTA K12
+    // K12c (k12.cu) is the fused path; BGS_K12C=0 falls back to the single-CTA K12
     const char* e2 = getenv("BGS_K12C");
-    no_k12c = !(e2 && *e2 && *e2 != '0');
+    no_k12c = e2 && *e2 == '0';
+    const char* e3 = getenv("BGS_PROF_STEP");
+    prof_step = e3 && *e3 && *e3 != '0';
     const char* d = getenv("BGS_TILE_DBG");
     tile_dbg = d ? atoi(d) : 0;
     const char* tp = getenv("BGS_TILE_PROF");
@@ -476,8 +479,12 @@ class Runner {
     p.dbg = tile_dbg;
     if (!k12_plan(p)) return -1;
     for (auto& x : sh)
-      if (x.rows > 0 && grid_for(x) < 2) return -1;
-    if (tile_prof) {
+      if (x.rows > 0 && grid_for(x) < p.cluster) return -1;
+    static const int prof_minkp = [] {
+      const char* e = getenv("BGS_PROF_MINKP");
+      return e ? atoi(e) : 0;
+    }();
+    if (tile_prof && fz.kp >= prof_minkp) {
       c->metrics.ensure((size_t)512 * 16 * sizeof(unsigned long long) + 64);
       p.phase = reinterpret_cast<unsigned long long*>(c->metrics.p) + 256 * 16;
     }
@@ -485,14 +492,14 @@ class Runner {
     const size_t per_slot = gram_partial_doubles_per_cta(p.mt_out, p.N);
     int slot_base = 0;
     for (auto& x : sh) {
-      const int grid = grid_for(x) & ~1;
+      const int grid = p.cluster == 2 ? grid_for(x) & ~1 : grid_for(x);
       if (x.rows > 0) {
         for (int wi = 0; wi < 5; ++wi)
           p.map0[wi] = sp.sp[0].src == SX ? x.mapX[0][wi] : x.mapQ[0][wi];
         for (int wi = 0; wi < 2; ++wi)
           p.map1[wi] = sp.sp[1].src == SX ? x.mapX[0][3 + wi] : x.mapQ[0][3 + wi];
         p.n_rows = x.rows;
-        p.total_stages = (x.rows + 31) / 32;
+        p.total_stages = (x.rows + 32 * p.R - 1) / (32 * p.R);
         p.partial = c->partial.d() + per_slot * slot_base;
         p.dstA = x.Q + (size_t)fz.dstA * x.ldq;
         p.lddA = x.ldq;
@@ -501,9 +508,11 @@ class Runner {
         const int nout = (fz.a ? 1 : 0) + (fz.b ? 1 : 0);
         const double bytes = 8.0 * x.rows * (sp.sp[0].ncols + sp.sp[1].ncols) + 8.0 * x.rows * s * nout;
         const double flops = 2.0 * x.rows * (double)M * sp.N + 2.0 * x.rows * (double)fz.kp * s * nout;
-        Prof pr(c, "fused_update_gram", bytes, flops);
+        char cls[64] = "fused_update_gram";
+        if (prof_step) snprintf(cls, sizeof cls, "fused_update_gram@kp%04d", fz.kp);
+        Prof pr(c, cls, bytes, flops);
         CUDA_OK(k12_launch(p, grid, c->stream, &c->launches));
-        slot_base += grid;
+        slot_base += grid / p.cluster;
       } else {
         CUDA_OK(cudaMemsetAsync(c->partial.d() + per_slot * slot_base, 0,
                                 per_slot * sizeof(double), c->stream));
@@ -619,8 +628,10 @@ class Runner {
           flops_upd = 2.0 * x.rows * (double)fz->kp * s * nout;
         }
         const double bytes = 8.0 * x.rows * (sp.sp[0].ncols + (sp.nspans == 2 ? sp.sp[1].ncols : 0));
-        Prof pr(c, upd ? "fused_update_gram" : "gram", bytes + bytes_upd,
-                2.0 * x.rows * (double)M * sp.N + flops_upd);
+        char cls[64];
+        snprintf(cls, sizeof cls, "%s", upd ? "fused_update_gram" : "gram");
+        if (upd && prof_step) snprintf(cls, sizeof cls, "fused_update_gram@kp%04d", fz->kp);
+        Prof pr(c, cls, bytes + bytes_upd, 2.0 * x.rows * (double)M * sp.N + flops_upd);
         CUDA_OK(tile_launch(p, upd, grid, c->stream, &c->launches));
       } else {
         CUDA_OK(cudaMemsetAsync(c->partial.d() + per_cta * cta_base, 0,

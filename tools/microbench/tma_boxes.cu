@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(160, 1) stream(const __grid_constant__ P p, do
               asm volatile(
                   "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                   ::"r"(su32(dst + (size_t)(br * p.boxes_c + bc) * box_bytes)), "l"((uint64_t)&p.map),
-                  "r"(0), "r"((row + br * p.rows_per_box) / 16), "r"(bc * p.cols_per_box), "r"(su32(&full[slot])) : "memory");
+                  "r"(0), "r"(p.dims3 == 2 ? bc * p.cols_per_box : (row + br * p.rows_per_box) / 16),
+                  "r"(p.dims3 == 2 ? (row + br * p.rows_per_box) / 16 : bc * p.cols_per_box), "r"(su32(&full[slot])) : "memory");
             else
               asm volatile(
                   "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -94,20 +95,27 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   struct Cfg { int rpb, cpb, swz, d3; };
-  std::vector<Cfg> cfgs = {{32, 64, 0, 0}, {32, 64, 1, 1}, {32, 32, 1, 1}, {32, 16, 1, 1}, {32, 8, 1, 1}, {64, 64, 1, 1}, {64, 32, 1, 1}, {32, 128, 1, 1}};
+  // d3 = 1: view {16 rows, row-blocks, cols}; d3 = 2: view {16 rows, cols, row-blocks}
+  // (smem lines ordered column-major within each 16-row block)
+  std::vector<Cfg> cfgs = {{32, 64, 1, 1}, {32, 128, 1, 1}, {32, 64, 1, 2}, {32, 128, 1, 2},
+                           {32, 32, 1, 2}, {64, 64, 1, 2}, {64, 128, 1, 2}};
   for (long C : {128L, 384L}) {
     for (auto cf : cfgs) {
       if (C % cf.cpb) continue;
-      for (int S : {2, 4}) {
+      for (int S : {2, 3, 4}) {
         P p;
         cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)C, 0};
         cuuint64_t str[2] = {(cuuint64_t)n * 8, 0};
         cuuint32_t box[3] = {(cuuint32_t)cf.rpb, (cuuint32_t)cf.cpb, 0};
         cuuint32_t es[3] = {1, 1, 1};
-        if (cf.d3) {
+        if (cf.d3 == 1) {
           dims[0] = 16; dims[1] = n / 16; dims[2] = C;
           str[0] = 128; str[1] = n * 8;
           box[0] = 16; box[1] = cf.rpb / 16; box[2] = cf.cpb;
+        } else if (cf.d3 == 2) {
+          dims[0] = 16; dims[1] = C; dims[2] = n / 16;
+          str[0] = n * 8; str[1] = 128;
+          box[0] = 16; box[1] = cf.cpb; box[2] = cf.rpb / 16;
         }
         p.dims3 = cf.d3;
         CUresult r = enc(&p.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cf.d3 ? 3 : 2, x, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
