@@ -23,6 +23,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <random>
 #include <string>
 #include <vector>
@@ -200,6 +201,9 @@ struct bgs_ctx {
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // copy engines of the host drop-in (bgs_factor): X chunks in, final Q columns out
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> xfer_events;  // reusable, timing disabled
   DBuf partial, G, scolA, scolB, sdiag, ydiag, save, r1, r2, rtop, R, status;
   DBuf tsqr_ws, tsqr_bounds, tsqr_trees, roots, roots_all, cross_ws, cross_m, metrics;
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
@@ -259,6 +263,9 @@ struct bgs_ctx {
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
+    for (auto e : xfer_events) cudaEventDestroy(e);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -335,6 +342,27 @@ class Runner {
     tile_dbg = d ? atoi(d) : 0;
     const char* tp = getenv("BGS_TILE_PROF");
     tile_prof = tp && *tp && *tp != '0';
+  }
+
+  // Streaming hooks of the host drop-in (bgs_factor): X arrives in column chunks on a copy
+  // stream (the compute stream waits on a chunk's event before the first kernel that reads
+  // it) and Q columns leave on another copy stream as soon as they are final.
+  struct XFeed {
+    long chunk_cols = 0;
+    std::vector<cudaEvent_t> ready;  // per chunk, recorded on the H2D stream
+    int waited = 0;                  // chunks the compute stream already waits on
+  };
+  XFeed* feed = nullptr;
+  std::function<void(long)> on_q_final;  // Q columns [0, c) are final
+  void need_x(long col_end) {
+    if (!feed || col_end <= 0) return;
+    const int upto = (int)std::min<long>((long)feed->ready.size(),
+                                         (col_end + feed->chunk_cols - 1) / feed->chunk_cols);
+    for (; feed->waited < upto; ++feed->waited)
+      CUDA_OK(cudaStreamWaitEvent(c->stream, feed->ready[feed->waited], 0));
+  }
+  void q_final(long col_end) {
+    if (on_q_final) on_q_final(col_end);
   }
 
   // RAII bracket of one launch (or launch group) of a kernel class for the profiler.
@@ -544,6 +572,8 @@ class Runner {
   // Returns M (rows of the compact Gram written to c->G, ld = M).
   int gram(const GramSpec& sp, const char* label, bool count_sync = true,
            bool do_allreduce = true, const Fuse* fz = nullptr) {
+    for (int i = 0; i < sp.nspans; ++i)
+      if (sp.sp[i].src == SX) need_x(sp.sp[i].col0 + sp.sp[i].ncols);
     TileParams p;
     memset(&p, 0, sizeof p);
     int units[2] = {0, 0}, lc[2] = {0, 0};
@@ -663,6 +693,8 @@ class Runner {
     const double* CB = nullptr; long ldcb = 0; const double* TB = nullptr;
   };
   void update(const Upd& u) {
+    if (u.has_a && u.srcA == SX) need_x(u.colA + s);
+    if (u.has_b && u.srcB == SX) need_x(u.colB + s);
     for (auto& x : sh) {
       if (x.rows <= 0) continue;
       UpdateParams p;
@@ -712,6 +744,7 @@ class Runner {
   // rendezvous (tsqr_fused_gram, intraorth.cpp:122-135).
   void tsqr(int src, long scol_, long dcol, double* rout, int ldrout, const char* label,
             long fused_words = 0, double* fusedG = nullptr) {
+    if (src == SX) need_x(scol_ + s);
     const size_t ss = (size_t)s * s;
     double* ws = c->tsqr_ws.d();
     const long* bounds = static_cast<const long*>(c->tsqr_bounds.p);
@@ -897,6 +930,7 @@ class Runner {
         u.srcA = SQ; u.colA = kp; u.dstA = kp;
         u.CA = c->G.d(); u.ldca = M; u.TA = ydiag;
         update(u);
+        q_final(m);
         break;
       }
       // Q_k = (U_k - Q_{1:k} Y) Y_kk^{-1}; U_{k+1} = (X_{k+1} - Q_{1:k+1} [Z; S2]) S^{-1};
@@ -928,6 +962,7 @@ class Runner {
         if (mode == OS_TSQR) tsqr(SQ, kp + si, kp + si, sdiag, si, "reduce_factor_tree:tsqr");
         M = gram(onesync_spec_unfused(mode, k + 1), lab);
       }
+      q_final(kp + si);  // later steps only write columns >= kp + s
       std::swap(scol_cur, scol_nxt);
     }
   }
@@ -1092,6 +1127,7 @@ class Runner {
       case BGS_BCGSI_PLUS_1S: onesync(OS_SKIP, 3); break;
       default: fail(BGS_E_CONFIG, "variant %d is out of scope", variant);
     }
+    q_final(m);
   }
 
   // Converts the device status word into the reference's exception semantics.
@@ -1337,6 +1373,18 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
     if (c->nranks > 1) fail(BGS_E_CONFIG, "bgs_factor runs on a single-GPU context; use bgs_factor_device per rank");
     select_device(c);
     Runner run(c, variant, n, m, s, procs, false, stats);
+    // Stream X in and Q out on copy engines, overlapped with the factorization, when both
+    // host buffers are pinned (pageable copies would block the enqueueing thread).
+    auto pinned = [](const void* p) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return a.type == cudaMemoryTypeHost;
+    };
+    const char* nsio = getenv("BGS_NO_STREAM_IO");
+    const bool stream_io = !(nsio && *nsio && *nsio != '0') && pinned(x) && pinned(q);
     c->sx.resize(std::max<size_t>(c->sx.size(), (size_t)procs));
     c->sq.resize(std::max<size_t>(c->sq.size(), (size_t)procs));
     for (int rk = 0; rk < procs; ++rk) {
@@ -1350,11 +1398,53 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
       c->sq[rk].ensure((size_t)sh.ldq * m * sizeof(double) + 256);
       sh.X = c->sx[rk].d();
       sh.Q = c->sq[rk].d();
-      if (rows > 0)
+      if (rows > 0 && !stream_io)
         CUDA_OK(cudaMemcpy2DAsync(c->sx[rk].p, sh.ldx * sizeof(double), x + r0, ldx * sizeof(double),
                                   rows * sizeof(double), m, cudaMemcpyHostToDevice, c->stream));
       CUDA_OK(cudaMemsetAsync(c->sq[rk].p, 0, (size_t)sh.ldq * m * sizeof(double), c->stream));
       run.sh.push_back(sh);
+    }
+    Runner::XFeed feed;
+    long q_done = 0;
+    if (stream_io) {
+      if (!c->h2d) CUDA_OK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+      if (!c->d2h) CUDA_OK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+      // chunks of whole blocks, ~16 columns (128 MB at n = 1e6)
+      feed.chunk_cols = s * std::max<long>(1, 16 / s);
+      const int nch = (int)((m + feed.chunk_cols - 1) / feed.chunk_cols);
+      const size_t need = (size_t)nch + (size_t)(m / feed.chunk_cols) + 4;
+      while (c->xfer_events.size() < need) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->xfer_events.push_back(e);
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        const long c0 = ch * feed.chunk_cols, nc = std::min(feed.chunk_cols, m - c0);
+        for (const Shard& sh : run.sh)
+          if (sh.rows > 0)
+            CUDA_OK(cudaMemcpy2DAsync(const_cast<double*>(sh.X) + (size_t)c0 * sh.ldx,
+                                      sh.ldx * sizeof(double), x + sh.row0 + (size_t)c0 * ldx,
+                                      ldx * sizeof(double), sh.rows * sizeof(double), nc,
+                                      cudaMemcpyHostToDevice, c->h2d));
+        CUDA_OK(cudaEventRecord(c->xfer_events[ch], c->h2d));
+        feed.ready.push_back(c->xfer_events[ch]);
+      }
+      run.feed = &feed;
+      size_t next_ev = (size_t)nch;
+      run.on_q_final = [&, next_ev](long cend) mutable {
+        if (cend <= q_done || (cend < m && cend - q_done < feed.chunk_cols)) return;
+        cudaEvent_t e = c->xfer_events[next_ev];
+        next_ev = next_ev + 1 < c->xfer_events.size() ? next_ev + 1 : (size_t)nch;
+        CUDA_OK(cudaEventRecord(e, c->stream));
+        CUDA_OK(cudaStreamWaitEvent(c->d2h, e, 0));
+        for (const Shard& sh : run.sh)
+          if (sh.rows > 0)
+            CUDA_OK(cudaMemcpy2DAsync(q + sh.row0 + (size_t)q_done * ldq, ldq * sizeof(double),
+                                      sh.Q + (size_t)q_done * sh.ldq, sh.ldq * sizeof(double),
+                                      sh.rows * sizeof(double), cend - q_done,
+                                      cudaMemcpyDeviceToHost, c->d2h));
+        q_done = cend;
+      };
     }
     c->launches = 0;
     CUDA_OK(cudaEventRecord(c->e0, c->stream));
@@ -1363,8 +1453,9 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaGetLastError());
     c->prof_resolve();
+    if (stream_io) CUDA_OK(cudaStreamSynchronize(c->d2h));
     run.check_status();
-    for (int rk = 0; rk < procs; ++rk) {
+    for (int rk = 0; rk < procs && !stream_io; ++rk) {
       const Shard& sh = run.sh[rk];
       if (sh.rows > 0)
         CUDA_OK(cudaMemcpy2DAsync(q + sh.row0, ldq * sizeof(double), sh.Q, sh.ldq * sizeof(double),
@@ -1383,6 +1474,8 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
     }
     return BGS_OK;
   } catch (const Fail& f) {
+    if (c && c->h2d) cudaStreamSynchronize(c->h2d);
+    if (c && c->d2h) cudaStreamSynchronize(c->d2h);
     if (c && c->stream) cudaStreamSynchronize(c->stream);
     put_err(err, f);
     return f.code;

@@ -257,3 +257,29 @@ def test_procs_change_only_rounding(oracle, gpu_ctx):
         o = bgs.run_factor(3, x, 4, p, metrics=False)
         assert o.stats.event_labels == base.stats.event_labels
         assert_r_close(o.r, base.r, 1e-12)
+
+
+@pytest.mark.parametrize("v,procs", [(3, 1), (3, 3), (2, 1), (4, 2), (1, 1)],
+                         ids=lambda p: str(p))
+def test_streamed_host_io_is_bitwise_identical(gpu_ctx, v, procs):
+    """bgs_factor with pinned host buffers streams X in / Q out on copy engines while the
+    sweep runs; the result must be bit-identical to the staged copy path."""
+    import ctypes
+    import torch
+    from paper_2507_21791_b200 import api
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 70001, 96, 4
+    x = bgs.gen_gaussian_host(777, n, m)
+    staged = bgs.run_factor(v, x, s, procs, metrics=False, ctx=gpu_ctx)
+    assert staged.ok
+    hx = torch.from_numpy(np.asfortranarray(x).T.copy()).pin_memory()  # (m, n) = column-major n x m
+    hq = torch.zeros((m, n), dtype=torch.float64).pin_memory()
+    r = np.zeros((m, m), order="F")
+    st, tm, err = api._Stats(), api._Timing(), api._Err()
+    rc = api._lib.bgs_factor(gpu_ctx.handle, v, n, m, s, procs, hx.data_ptr(), n, hq.data_ptr(),
+                             n, r.ctypes.data, m, ctypes.byref(st), ctypes.byref(tm),
+                             ctypes.byref(err))
+    api._raise(rc, err)
+    q = hq.numpy().T
+    assert np.array_equal(q, staged.q)
+    assert np.array_equal(r, staged.r)
