@@ -443,15 +443,18 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant
   }
 }
 
-// Deterministic cross-CTA reduction in double-double, rank-local.  A CTA handles 32
-// output entries with 8 slices each: slice l sums CTA partials g = l, l+8, ... in order,
-// then the 8 slice sums are combined in slice order.  Fixed order -> reproducible.
-constexpr int RED_ENTRIES = 32, RED_SLICES = 8;
+// Deterministic cross-CTA reduction in double-double, rank-local.  A CTA handles 16
+// output entries with 16 slices each: slice l sums partials g = l, l+16, ... in order
+// (8 independent loads in flight per thread), then the 16 slice sums are combined in
+// slice order.  Fixed order -> reproducible.
+constexpr int RED_ENTRIES = 16, RED_SLICES = 16, RED_BATCH = 8;
 __global__ void __launch_bounds__(RED_ENTRIES * RED_SLICES)
     gram_reduce_kernel(const double2* __restrict__ part, int G, int mt_out, int N8, int N,
                        int ubox0, int lcols0, int lcols1, int M, double* __restrict__ out,
                        const DevStatus* status) {
-  if (status && status_bad(status)) return;
+  // (no status check: after a failure the next small op returns first, and skipping
+  // it here saves a dependent global load in front of the partial loads)
+  (void)status;
   __shared__ double2 red[RED_SLICES][RED_ENTRIES];
   const int le = threadIdx.x % RED_ENTRIES, sl = threadIdx.x / RED_ENTRIES;
   const int idx = blockIdx.x * RED_ENTRIES + le;
@@ -459,13 +462,20 @@ __global__ void __launch_bounds__(RED_ENTRIES * RED_SLICES)
   double s = 0.0, e = 0.0;
   if (idx < per_cta) {
     const double2* ptr = part + idx;
-#pragma unroll 4
-    for (int g = sl; g < G; g += RED_SLICES) {
-      const double2 v = ptr[(size_t)g * per_cta];
-      double s2, err;
-      two_sum(s, v.x, s2, err);
-      s = s2;
-      e += err + v.y;
+    for (int g0 = sl; g0 < G; g0 += RED_SLICES * RED_BATCH) {
+      double2 v[RED_BATCH];
+#pragma unroll
+      for (int u = 0; u < RED_BATCH; ++u) {
+        const int g = g0 + u * RED_SLICES;
+        v[u] = g < G ? __ldg(ptr + (size_t)g * per_cta) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < RED_BATCH; ++u) {  // adding (0, 0) leaves (s, e) unchanged
+        double s2, err;
+        two_sum(s, v[u].x, s2, err);
+        s = s2;
+        e += err + v[u].y;
+      }
     }
   }
   red[sl][le] = make_double2(s, e);

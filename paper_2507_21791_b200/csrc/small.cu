@@ -316,8 +316,256 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------------
+// SM_ONESYNC_STEP for s <= 4 (bcgs.cpp:294-367), the per-step op of the one-sync sweep:
+// one pass over the kp rows of [Y | Z] = G[0:kp, 0:2s] computes Y^T Y, Y^T Z, Z^T Z (36
+// dot products per thread, then a fixed-order block reduction), the R column
+// S_prev + Y S_diag and the copy of Z into scol_next; thread 0 then runs the s x s
+// Cholesky / triangular solves in registers.  Same operation order as chol_serial /
+// trsm_lt_serial / r_diag; only the kp-long sums are grouped differently (the reference
+// forms them sequentially, this path by rows-per-thread then a tree).
+// ---------------------------------------------------------------------------------
+namespace {
+constexpr int kStepThreads = 256;
+
+// upper Cholesky of the symmetrized 4x4 (s x s used) a into g; 1-based failing pivot
+BGS_DEV int chol4(const double (&a)[16], int s, double (&g)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) g[k] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int i = 0; i <= j; ++i) {
+      if (j < s) {
+        double acc = 0.5 * (a[i + 4 * j] + a[j + 4 * i]);
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * g[k + 4 * j];
+        if (i == j) {
+          if (!(acc > 0.0)) return j + 1;
+          g[j + 4 * j] = sqrt(acc);
+        } else {
+          g[i + 4 * j] = acc / g[i + 4 * i];
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+// w = g^{-T} b (g upper); 1-based index of a zero diagonal entry, else 0
+BGS_DEV int trsm4(const double (&g)[16], const double (&b)[16], int s, double (&w)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) w[k] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < s) {
+      const double gii = g[i + 4 * i];
+      if (gii == 0.0) return i + 1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < s) {
+          double acc = b[i + 4 * j];
+#pragma unroll
+          for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * w[k + 4 * j];
+          w[i + 4 * j] = acc / gii;
+        }
+      }
+    }
+  }
+  return 0;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kStepThreads, 1) onesync_step4_kernel(SmallParams p) {
+  const int s = p.s, kp = p.kp, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nz = p.has_next ? s : 0;  // Z columns present
+  __shared__ double red[kStepThreads / 32][36];
+  __shared__ double prod[36];
+  __shared__ int bad_flag;
+  if (tid == 0) bad_flag = 0;
+  // previous S_diag (broadcast loads) and the status word, issued together
+  double sdp[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) sdp[e] = ((e & 3) < s && (e >> 2) < s) ? p.sdiag[(e & 3) + s * (e >> 2)] : 0.0;
+  const bool dead = status_bad(p.status);
+  // ---- one pass over rows: products, R column, scol_next copy, non-finite check ----
+  double acc[36];
+#pragma unroll
+  for (int e = 0; e < 36; ++e) acc[e] = 0.0;
+  int bad = 0;
+  double rcol[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = tid + h * kStepThreads;
+    double y[4] = {0.0, 0.0, 0.0, 0.0}, z[4] = {0.0, 0.0, 0.0, 0.0};
+    if (r < kp) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        if (l < s) y[l] = p.G[r + (size_t)l * p.ldg];
+        if (l < nz) z[l] = p.G[r + (size_t)(s + l) * p.ldg];
+      }
+#pragma unroll
+      for (int l = 0; l < 4; ++l) bad |= !isfinite(y[l]) | !isfinite(z[l]);
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        // R(r, kp + l) = S_prev(r, l) + sum_m Y(r, m) S_diag(m, l)
+        double a = 0.0;
+#pragma unroll
+        for (int m2 = 0; m2 < 4; ++m2) a += y[m2] * sdp[m2 + 4 * l];
+        rcol[h][l] = l < s ? p.scol_prev[r + (size_t)l * p.ld_scol_prev] + a : 0.0;
+        if (l < nz) p.scol_next[r + (size_t)l * p.ld_scol_next] = z[l];
+      }
+    }
+    // packed upper YtY (10), full YtZ (16), upper ZtZ (10)
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i <= j; ++i, ++e) acc[e] = fma(y[i], y[j], acc[e]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i, ++e) acc[e] = fma(y[i], z[j], acc[e]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i <= j; ++i, ++e) acc[e] = fma(z[i], z[j], acc[e]);
+  }
+  // the rest of the reduced Gram, for the non-finite check (rows kp..gm)
+  for (int e = tid; e < (p.gm - kp) * p.gn; e += kStepThreads) {
+    const int r = kp + e % (p.gm - kp), c = e / (p.gm - kp);
+    bad |= !isfinite(p.G[r + (size_t)c * p.ldg]);
+  }
+  if (bad) atomicOr(&bad_flag, 1);
+#pragma unroll
+  for (int e = 0; e < 36; ++e) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int e = 0; e < 36; ++e) red[warp][e] = acc[e];
+  __syncthreads();
+  if (dead) return;
+  if (tid < 36) {
+    double t = 0.0;
+    for (int w = 0; w < kStepThreads / 32; ++w) t += red[w][tid];
+    prod[tid] = t;
+  }
+  if (bad_flag) {
+    if (tid == 0) set_status(p.status, ST_NON_FINITE, 0, p.k + 1, SITE_NONE, 0);
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = tid + h * kStepThreads;
+    if (r < kp)
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        if (l < s) p.R[r + (size_t)(kp + l) * p.ldr] = rcol[h][l];
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  // ---- thread 0: s x s factors in registers ----
+  const double* G = p.G;
+  const size_t ld = p.ldg;
+  double ytz[16], c[16], yd[16], sd[16];
+  {
+    int e = 0;
+    double yty[16];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i <= j; ++i) {
+        yty[i + 4 * j] = yty[j + 4 * i] = prod[e];
+        ++e;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ytz[i + 4 * j] = prod[e++];
+    // Y_diag = chol(Omega - Y^T Y)  (bcgs.cpp:321-327)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        c[i + 4 * j] = (i < s && j < s) ? G[(kp + i) + j * ld] - yty[i + 4 * j] : 0.0;
+  }
+  int piv = chol4(c, s, yd);
+  if (piv) {
+    set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if ((e & 3) < s && (e >> 2) < s) p.ydiag[(e & 3) + s * (e >> 2)] = yd[e];
+  // R_kk = upper_product(Y_diag, S_diag)  (bcgs.cpp:35-49, 333)
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (i < s && j < s) {
+        double a = 0.0;
+        if (i <= j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k >= i && k <= j) a += yd[i + 4 * k] * sdp[k + 4 * j];
+        p.R[(kp + i) + (size_t)(kp + j) * p.ldr] = i <= j ? a : 0.0;
+      }
+    }
+  if (!p.has_next) return;
+  // S2 = Y_diag^{-T} (P - Y^T Z); scol_next = [Z; S2]  (bcgs.cpp:336-344)
+  double bm[16], s2[16];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      bm[i + 4 * j] = (i < s && j < s) ? G[(kp + i) + (s + j) * ld] - ytz[i + 4 * j] : 0.0;
+  piv = trsm4(yd, bm, s, s2);
+  if (piv) {
+    set_status(p.status, ST_SINGULAR, piv, p.k + 1, SITE_NONE, 0);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < s && j < s) p.scol_next[(kp + i) + (size_t)j * p.ld_scol_next] = s2[i + 4 * j];
+  if (p.os_mode == OS_PYTH) {
+    // S_diag = chol(T - scol^T scol), scol^T scol = Z^T Z + S2^T S2  (bcgs.cpp:352-359)
+    double t[16];
+    int e = 26;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i <= j; ++i) {
+        double a = prod[e++];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a += s2[k + 4 * i] * s2[k + 4 * j];
+        const double v = (i < s && j < s) ? G[(kp + s + i) + (s + j) * ld] : 0.0;
+        const double vt = (i < s && j < s) ? G[(kp + s + j) + (s + i) * ld] : 0.0;
+        t[i + 4 * j] = v - a;
+        t[j + 4 * i] = vt - a;
+      }
+    piv = chol4(t, s, sd);
+    if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 2, SITE_FIRST_PASS, p.kappa_power);
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if ((k & 3) < s && (k >> 2) < s) p.sdiag[(k & 3) + s * (k >> 2)] = sd[k];
+  } else if (p.os_mode == OS_SKIP) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if ((k & 3) < s && (k >> 2) < s) p.sdiag[(k & 3) + s * (k >> 2)] = (k & 3) == (k >> 2) ? 1.0 : 0.0;
+  }
+}
+
 cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches) {
   if (p.s < 1 || p.s > SMAX) return cudaErrorInvalidValue;
+  if (p.mode == SM_ONESYNC_STEP && p.s <= 4 && p.kp <= 2 * kStepThreads && !p.sdiag_prev_copy) {
+    onesync_step4_kernel<<<1, kStepThreads, 0, st>>>(p);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
   const size_t smem =
       ((size_t)(p.gm > 0 ? p.gm * p.gn : 0) + (size_t)p.kp * p.s + (size_t)(p.kp + p.s) * p.s) *
       sizeof(double);
