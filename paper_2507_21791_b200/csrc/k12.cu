@@ -523,11 +523,9 @@ bool k12_plan(SplitParams& p) {
   p.mt_out = p.U0 + p.s1_left;
   // C = 1 with the tallest stage that keeps >= 3 stages in shared memory, then the pair
   const Cand cands[] = {{1, 4}, {1, 2}, {1, 1}, {2, 2}, {2, 1}};
-  // BGS_K12C_PLAN=CR (e.g. 21): only that candidate (experiments)
-  static const int forced = [] {
-    const char* e = getenv("BGS_K12C_PLAN");
-    return e ? atoi(e) : 0;
-  }();
+  // BGS_K12C_PLAN=CR (e.g. 21): only that candidate (tests / experiments; read per call)
+  const char* fe = getenv("BGS_K12C_PLAN");
+  const int forced = fe ? atoi(fe) : 0;
   for (const Cand& cd : cands) {
     if (forced && forced != 10 * cd.C + cd.R) continue;
     SplitParams q = p;

@@ -283,3 +283,34 @@ def test_streamed_host_io_is_bitwise_identical(gpu_ctx, v, procs):
     q = hq.numpy().T
     assert np.array_equal(q, staged.q)
     assert np.array_equal(r, staged.r)
+
+
+@pytest.mark.parametrize("plan", ["14", "12", "11", "22", "21"])
+@pytest.mark.parametrize("v", [3, 2, 5], ids=lambda v: NAMES[v])
+def test_fused_plans_match_oracle(oracle, gpu_ctx, monkeypatch, v, plan):
+    """Every K12c plan (cluster width C, 32-row chunks per stage R; BGS_K12C_PLAN=CR)
+    against the oracle, with a ragged n so the last stage is partial.  Steps the forced
+    plan cannot take fall back to the single-CTA K12."""
+    import paper_2507_21791_b200 as bgs
+    monkeypatch.setenv("BGS_K12C_PLAN", plan)
+    n, m, s = 20011, 96, 4
+    x = oracle.gen_matrix(n, m, s, 1e3, 4242, False)
+    ref = oracle.factor(v, x, s, 1, metrics=True)
+    out = bgs.run_factor(v, x, s, 1, metrics=False)
+    assert out.ok, out.error
+    assert out.stats.event_labels == ref.labels
+    assert_structure(out.r)
+    assert_r_close(out.r, ref.r)
+    assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
+    assert oracle.residual(x, out.q, out.r) <= 10 * max(ref.resid, U)
+
+
+def test_fused_plans_agree_bitwise_across_procs_splits(gpu_ctx, monkeypatch):
+    """The CTA-pair plans form D_0 + D_1 on both ranks: results are deterministic run to
+    run (bitwise) for a fixed plan."""
+    import paper_2507_21791_b200 as bgs
+    monkeypatch.setenv("BGS_K12C_PLAN", "21")
+    x = bgs.gen_gaussian_host(99, 30001, 128)
+    a = bgs.run_factor(3, x, 4, 1, metrics=False)
+    b = bgs.run_factor(3, x, 4, 1, metrics=False)
+    assert np.array_equal(a.q, b.q) and np.array_equal(a.r, b.r)
