@@ -26,7 +26,7 @@ from typing import Dict, List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbgs_gpu.so")
+LIB_PATH = os.environ.get("BGS_LIB_PATH") or os.path.join(_HERE, "_lib", "libbgs_gpu.so")  # override: A/B builds
 
 # ---------------------------------------------------------------------------------------
 # errors (errors.hpp:9-51) — codes shared with include/bgs_gpu.h
