@@ -613,13 +613,14 @@ cudaError_t tile_launch(TileParams& p, bool upd, int grid, cudaStream_t st, int*
 }
 
 cudaError_t gram_reduce_launch(const TileParams& p, int ctas, double* out, cudaStream_t st,
-                               int* launches) {
+                               int* launches, int ld_out) {
   const int N8 = 8 * gram_n_tiles(p.N);
   const int entries = p.mt_out * 8 * N8;
   const int lc1 = p.mt_out > p.units_span[0] ? p.lcols[1] : 0;
   gram_reduce_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, RED_ENTRIES * RED_SLICES, 0,
                        st>>>(reinterpret_cast<const double2*>(p.partial), ctas, p.mt_out, N8, p.N,
-                             p.units_span[0], p.lcols[0], lc1, p.lcols[0] + lc1, out, p.status);
+                             p.units_span[0], p.lcols[0], lc1,
+                             ld_out > 0 ? ld_out : p.lcols[0] + lc1, out, p.status);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

@@ -561,8 +561,10 @@ bool k12_plan(SplitParams& p) {
     int kw_t = std::max(2, (kw + 1) / 2 * 2);
     while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) kw_t += 2;
     if (kw_t > kw_max) continue;
+    const char* me = getenv("BGS_K12C_MINS");  // experiments: minimum ring depth (default 3)
+    const int min_s = me ? std::max(2, atoi(me)) : 3;
     int S = 0;
-    for (int st = kMaxStages; st >= 3; --st)
+    for (int st = kMaxStages; st >= min_s; --st)
       if (k12_smem_bytes(st, q.slot_units, cd.R, cd.C) + kStaticSmem + 256 <= (size_t)kSmemOptin) {
         S = st;
         break;

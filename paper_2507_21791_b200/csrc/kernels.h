@@ -56,8 +56,9 @@ bool tile_fused_supported(int s, int kp, int mt_out);
 size_t tile_smem_bytes(int H, int stages, int units, bool upd);
 // Deterministic double-double sum over `ctas` partial slots -> compact M x N Gram
 // (M = lcols[0] + lcols[1]).
+// ld_out > 0: write into a larger Gram (column stride ld_out; chunked left operands)
 cudaError_t gram_reduce_launch(const TileParams& p, int ctas, double* out, cudaStream_t st,
-                               int* launches);
+                               int* launches, int ld_out = 0);
 int gram_n_tiles(int N);
 size_t gram_partial_doubles_per_cta(int mt_out, int N);
 

@@ -207,6 +207,7 @@ struct bgs_ctx {
   DBuf partial, G, scolA, scolB, sdiag, ydiag, save, r1, r2, rtop, R, status;
   DBuf tsqr_ws, tsqr_bounds, tsqr_trees, roots, roots_all, cross_ws, cross_m, metrics;
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
+  std::vector<DBuf> rscr;    // per-shard right-operand scratch of chunked Grams
   int launches = 0;
   // live profiler: event pairs per launch, resolved after the stream syncs
   struct ProfClass {
@@ -254,6 +255,7 @@ struct bgs_ctx {
                     &cross_m, &metrics})
       b->release();
     for (auto& b : sx) b.release();
+    for (auto& b : rscr) b.release();
     for (auto& b : sq) b.release();
     for (auto& p : pending) {
       event_pool.push_back(p.a);
@@ -272,6 +274,8 @@ struct bgs_ctx {
 
 namespace {
 
+static long even_ld(long rows) { return std::max<long>(32, (rows + 31) & ~31L); }
+
 // One row shard resident on this device: rows [row0, row0 + rows) of the global matrix.
 struct Shard {
   long row0 = 0, rows = 0;
@@ -281,6 +285,10 @@ struct Shard {
   long ldq = 0;
   // tile-engine views: [H index: 0 -> H=2, 1 -> H=4][box width 128/64/32/16/8]
   CUtensorMap mapX[2][5], mapQ[2][5];
+  // chunked Grams: the right operand copied to a contiguous scratch (SR spans)
+  double* Rs = nullptr;
+  long ldr = 0;
+  CUtensorMap mapR[2][5];
   void make_maps(long m) {
     for (int hi = 0; hi < 2; ++hi)
       for (int wi = 0; wi < 5; ++wi) {
@@ -293,7 +301,7 @@ struct Shard {
   long hmax = 0;
 };
 
-enum Src { SX = 0, SQ = 1 };
+enum Src { SX = 0, SQ = 1, SR = 2 };  // X, Q, right-operand scratch (chunked Grams)
 
 struct GSpan {
   int src = SQ;
@@ -326,6 +334,7 @@ class Runner {
   bool no_fuse = false;
   bool no_k12c = false;
   bool prof_step = false;  // BGS_PROF_STEP: one profiler class per fused block step
+  int gram_max_units = 0;  // BGS_GRAM_MAXUNITS (tests): chunk unfused Grams above this
   int tile_dbg = 0;
   bool tile_prof = false;
 
@@ -338,6 +347,8 @@ class Runner {
     no_k12c = e2 && *e2 == '0';
     const char* e3 = getenv("BGS_PROF_STEP");
     prof_step = e3 && *e3 && *e3 != '0';
+    const char* e4 = getenv("BGS_GRAM_MAXUNITS");
+    gram_max_units = e4 ? atoi(e4) : 0;
     const char* d = getenv("BGS_TILE_DBG");
     tile_dbg = d ? atoi(d) : 0;
     const char* tp = getenv("BGS_TILE_PROF");
@@ -480,34 +491,41 @@ class Runner {
 
   // K12c (k12.cu): the fused update + Gram split over CTA pairs.  Returns -1 when the
   // shape is not covered (the caller then uses the single-CTA tile engine).
-  int gram_split(const GramSpec& sp, const char* label, bool count_sync, bool do_allreduce,
-                 const Fuse& fz, const int units[2], const int lc[2]) {
-    if (sp.nspans != 2 || sp.N > 8 || lc[0] != sp.sp[0].ncols) return -1;
-    SplitParams p;
+  // Structural K12c parameters of a fused Gram spec + the plan; false if K12c cannot run it.
+  bool split_params(const GramSpec& sp, bool a, bool b, int kp, SplitParams& p) const {
     memset(&p, 0, sizeof p);
+    if (no_k12c || sp.nspans != 2 || sp.N > 8 || sp.sp[0].lcols != sp.sp[0].ncols) return false;
     for (int j = 0; j < sp.N; ++j) {
-      if (sp.rspan[j] != 1) return -1;
+      if (sp.rspan[j] != 1) return false;
       p.rcol1[j] = sp.rcol[j];
     }
     for (int j = sp.N; j < 8; ++j) p.rcol1[j] = -1;
     p.N = sp.N;
-    p.U0 = units[0];
-    p.U1 = units[1];
+    p.U0 = (sp.sp[0].ncols + 7) / 8;
+    p.U1 = (sp.sp[1].ncols + 7) / 8;
     p.ncols0 = sp.sp[0].ncols;
-    p.lcols1 = lc[1];
+    p.lcols1 = sp.sp[1].lcols;
     p.col0[0] = sp.sp[0].col0;
     p.col0[1] = sp.sp[1].col0;
-    p.upd_a = fz.a;
-    p.upd_b = fz.b;
-    p.kp = fz.kp;
+    p.upd_a = a;
+    p.upd_b = b;
+    p.kp = kp;
     p.s = (int)s;
+    if (!k12_plan(p)) return false;
+    for (auto& x : sh)
+      if (x.rows > 0 && grid_for(x) < p.cluster) return false;
+    return true;
+  }
+
+  int gram_split(const GramSpec& sp, const char* label, bool count_sync, bool do_allreduce,
+                 const Fuse& fz, const int units[2], const int lc[2]) {
+    SplitParams p;
+    if (!split_params(sp, fz.a, fz.b, fz.kp, p)) return -1;
     p.CA = fz.CA; p.ldca = fz.ldca; p.TA = fz.TA;
     p.CB = fz.CB; p.ldcb = fz.ldcb; p.TB = fz.TB;
     p.status = status;
     p.dbg = tile_dbg;
-    if (!k12_plan(p)) return -1;
-    for (auto& x : sh)
-      if (x.rows > 0 && grid_for(x) < p.cluster) return -1;
+    (void)units;
     static const int prof_minkp = [] {
       const char* e = getenv("BGS_PROF_MINKP");
       return e ? atoi(e) : 0;
@@ -569,6 +587,72 @@ class Runner {
     return M;
   }
 
+  static const CUtensorMap& map_of(const Shard& x, int src, int hi, int wi) {
+    return src == SX ? x.mapX[hi][wi] : src == SQ ? x.mapQ[hi][wi] : x.mapR[hi][wi];
+  }
+  double* gout = nullptr;  // chunked Grams: where this chunk's rows go (ld gout_ld)
+  int gout_ld = 0;
+
+  // A left operand wider than one CTA's shared memory holds (H = 2, 2 stages; e.g. m = 800):
+  // copy the right operand (<= 32 columns) into a contiguous scratch, run the tile engine
+  // over column chunks of the left operand, each chunk writing its rows of the Gram; then
+  // one allreduce / sync record for the whole Gram, as before.
+  int gram_chunked(const GramSpec& sp, const char* label, bool count_sync, bool do_allreduce) {
+    const int N = sp.N;
+    struct Run {
+      int src, col0, n;
+    };
+    std::vector<Run> left;
+    int M = 0;
+    for (int i = 0; i < sp.nspans; ++i)
+      if (sp.sp[i].lcols > 0) {
+        left.push_back({sp.sp[i].src, sp.sp[i].col0, sp.sp[i].lcols});
+        M += sp.sp[i].lcols;
+      }
+    for (int j = 0; j < N; ++j)
+      if (sp.sp[sp.rspan[j]].src == SX) need_x(sp.sp[sp.rspan[j]].col0 + sp.rcol[j] + 1);
+    if (c->rscr.size() < sh.size()) c->rscr.resize(sh.size());
+    for (size_t i = 0; i < sh.size(); ++i) {
+      Shard& x = sh[i];
+      if (x.rows <= 0) continue;
+      x.ldr = even_ld(x.rows);
+      c->rscr[i].ensure((size_t)x.ldr * 32 * sizeof(double) + 256);
+      x.Rs = c->rscr[i].d();
+      for (int j = 0; j < N; ++j) {
+        const GSpan& g = sp.sp[sp.rspan[j]];
+        CUDA_OK(copy_cols_launch(colp(x, g.src, g.col0 + sp.rcol[j]), g.src == SX ? x.ldx : x.ldq,
+                                 x.Rs + (size_t)j * x.ldr, x.ldr, x.rows, 1, c->stream));
+      }
+      for (int hi = 0; hi < 2; ++hi)
+        for (int wi = 0; wi < 5; ++wi) x.mapR[hi][wi] = make_map3(x.Rs, x.rows, N, x.ldr, 2 << hi, 128 >> wi);
+    }
+    const int runits = (N + 7) / 8;
+    int cu = 1;
+    while (tile_smem_bytes(2, 2, cu + 1 + runits, false) <= (size_t)TILE_SMEM_MAX) ++cu;
+    if (gram_max_units > runits) cu = std::min(cu, gram_max_units - runits);
+    const int cw = 8 * cu;
+    int row_off = 0;
+    for (const Run& r : left)
+      for (int c0 = 0; c0 < r.n; c0 += cw) {
+        const int len = std::min(cw, r.n - c0);
+        GramSpec g = spec2(r.src, r.col0 + c0, len, len, SR, 0, N, 0);
+        add_right(g, 1, 0, N);
+        gout = c->G.d() + row_off;
+        gout_ld = M;
+        gram(g, "", false, false);
+        gout = nullptr;
+        gout_ld = 0;
+        row_off += len;
+      }
+    if (use_nccl && do_allreduce) {
+      Prof pr(c, "nccl_allreduce", (double)M * N * 8.0, 0.0);
+      NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * N, ncclDouble, ncclSum, c->comm,
+                               c->stream));
+    }
+    if (count_sync) record(label, (long)M * N);
+    return M;
+  }
+
   // Returns M (rows of the compact Gram written to c->G, ld = M).
   int gram(const GramSpec& sp, const char* label, bool count_sync = true,
            bool do_allreduce = true, const Fuse* fz = nullptr) {
@@ -601,7 +685,10 @@ class Runner {
       p.phase = reinterpret_cast<unsigned long long*>(c->metrics.p);
     }
     const bool upd = fz != nullptr;
-    if (upd && !no_k12c) {
+    if (!upd && !gout && (tile_smem_bytes(2, 2, p.units, false) > (size_t)TILE_SMEM_MAX ||
+                          (gram_max_units > 0 && p.units > gram_max_units)))
+      return gram_chunked(sp, label, count_sync, do_allreduce);
+    if (upd) {
       const int M = gram_split(sp, label, count_sync, do_allreduce, *fz, units, lc);
       if (M >= 0) return M;
     }
@@ -641,11 +728,9 @@ class Runner {
     for (auto& x : sh) {
       const int grid = grid_for(x);
       if (x.rows > 0) {
-        for (int wi = 0; wi < 5; ++wi)
-          p.map0[wi] = sp.sp[0].src == SX ? x.mapX[hi][wi] : x.mapQ[hi][wi];
+        for (int wi = 0; wi < 5; ++wi) p.map0[wi] = map_of(x, sp.sp[0].src, hi, wi);
         if (sp.nspans == 2)
-          for (int wi = 0; wi < 2; ++wi)
-            p.map1[wi] = sp.sp[1].src == SX ? x.mapX[hi][3 + wi] : x.mapQ[hi][3 + wi];
+          for (int wi = 0; wi < 2; ++wi) p.map1[wi] = map_of(x, sp.sp[1].src, hi, 3 + wi);
         p.n_rows = x.rows;
         p.partial = c->partial.d() + per_cta * cta_base;
         if (upd) {
@@ -672,7 +757,8 @@ class Runner {
     p.partial = c->partial.d();
     {
       Prof pr(c, "gram_reduce", (double)cta_base * per_cta * 8.0, 0.0);
-      CUDA_OK(gram_reduce_launch(p, cta_base, c->G.d(), c->stream, &c->launches));
+      CUDA_OK(gram_reduce_launch(p, cta_base, gout ? gout : c->G.d(), c->stream, &c->launches,
+                                 gout ? gout_ld : 0));
     }
     if (use_nccl && do_allreduce) {
       Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
@@ -823,8 +909,11 @@ class Runner {
     const bool span1_left = g.nspans == 2 && g.sp[1].lcols > 0;
     const int mt_out = span1_left ? (g.sp[0].ncols + 7) / 8 + (g.sp[1].lcols + 7) / 8
                                   : (g.sp[0].lcols + 7) / 8;
-    return tile_fused_supported((int)s, kp, mt_out) &&
-           tile_smem_bytes(2, 2, units, true) <= (size_t)TILE_SMEM_MAX;
+    if (tile_fused_supported((int)s, kp, mt_out) &&
+        tile_smem_bytes(2, 2, units, true) <= (size_t)TILE_SMEM_MAX)
+      return true;
+    SplitParams p;  // K12c can take shapes the single-CTA K12 cannot (CTA pairs)
+    return split_params(g, true, true, kp, p);
   }
 
   // Gram of one-sync step j over [Q_{1:j} U_j (X_{j+1})] when U_j already sits in Q
@@ -1184,7 +1273,6 @@ void select_device(bgs_ctx* c) { CUDA_OK(cudaSetDevice(c->device)); }
 
 // Leading dimension of library-owned device buffers: rows rounded up to 32 (the tile
 // engine's TMA view reads whole 16-row blocks; 32 keeps 256-byte column alignment).
-static long even_ld(long rows) { return std::max<long>(32, (rows + 31) & ~31L); }
 
 // =====================================================================================
 // C ABI
