@@ -167,6 +167,13 @@ inline double* tsqr_ws_M(double* ws, int L, int s) { return ws + (size_t)2 * L *
 cudaError_t tsqr_leaf_launch(const double* src, long lds, double* dst, long ldd,
                              const long* d_bounds, int L, long hmax, int s, double* rleaf,
                              const DevStatus* status, cudaStream_t st, int* launches);
+// Grouped tree of one shard's leaves [leaf_base, leaf_base + Lt): up -> root_out; down from
+// mtop (identity if null) -> the leaf M's (tsqr.cu).
+cudaError_t tsqr_tree_up_shard(double* ws, int L, int leaf_base, int Lt, int s, double* root_out,
+                               const DevStatus* status, cudaStream_t st, int* launches);
+cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s,
+                                 const double* mtop, const DevStatus* status, cudaStream_t st,
+                                 int* launches);
 // Bottom-up combine of every tree t (leaves [tree_off[t], tree_off[t+1])) -> roots + t*s*s.
 cudaError_t tsqr_up_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
                            double* roots, const DevStatus* status, cudaStream_t st,

@@ -834,7 +834,6 @@ class Runner {
     const size_t ss = (size_t)s * s;
     double* ws = c->tsqr_ws.d();
     const long* bounds = static_cast<const long*>(c->tsqr_bounds.p);
-    const int* trees = static_cast<const int*>(c->tsqr_trees.p);
     for (auto& x : sh) {
       Prof pr(c, "tsqr_leaf", 16.0 * x.rows * s, 8.0 * x.rows * s * s);
       CUDA_OK(tsqr_leaf_launch(colp(x, src, scol_), src == SX ? x.ldx : x.ldq, qcol(x, dcol),
@@ -844,8 +843,9 @@ class Runner {
     }
     {
       Prof pr(c, "tsqr_tree", 0.0, 0.0);
-      CUDA_OK(tsqr_up_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, c->roots.d(), status,
-                             c->stream, &c->launches));
+      for (size_t t = 0; t < sh.size(); ++t)
+        CUDA_OK(tsqr_tree_up_shard(ws, tsqr_L, sh[t].leaf_base, sh[t].n_leaves, (int)s,
+                                   c->roots.d() + t * ss, status, c->stream, &c->launches));
     }
     const double* all_roots = c->roots.d();
     if (use_nccl) {
@@ -862,8 +862,9 @@ class Runner {
       CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout,
                                 c->cross_m.d(), status, c->stream, &c->launches));
       const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
-      CUDA_OK(tsqr_down_launch((int)sh.size(), trees, ws, tsqr_L, (int)s, mtop, status, c->stream,
-                               &c->launches));
+      for (size_t t = 0; t < sh.size(); ++t)
+        CUDA_OK(tsqr_tree_down_shard(ws, tsqr_L, sh[t].leaf_base, sh[t].n_leaves, (int)s,
+                                     mtop + t * ss, status, c->stream, &c->launches));
     }
     for (auto& x : sh) {
       Prof pr(c, "tsqr_apply", 16.0 * x.rows * s, 2.0 * x.rows * s * s);

@@ -15,6 +15,11 @@
 //  apply kernel: Q rows of each leaf <- Q rows * M_leaf.
 // Every factor is carried as s x s (zero-padded rows for short leaves, which stack as
 // no-ops exactly like the reference's trapezoidal factors).
+#include <algorithm>
+#include <cstring>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -386,6 +391,182 @@ __global__ void tsqr_apply_kernel(double* dst, long ldd, const long* leaf_row0, 
       dst[i + (size_t)j * ldd] = acc;
     }
   }
+}
+
+// ---------------------------------------------------------------------------------
+// Grouped tree levels.  The tree pairs items level by level (pairs (2i, 2i+1); an odd last
+// item passes up), and pair i of level l is node nb[l] + i — the same numbering as
+// tree_up / tree_down.  A CTA takes 2^D consecutive items of level l0 and runs D levels in
+// shared memory (one warp per pair), so ~1000 leaves need two launches instead of one CTA
+// walking ten levels with ~30 serial pair QRs per warp at the bottom.
+// ---------------------------------------------------------------------------------
+struct TreeGroupArgs {
+  const double* in;   // level l0 items (up) / level l0 + D items (down), s x s each
+  double* out;        // level l0 + D items (up) / level l0 items (down)
+  double* nq;         // node Q factors of this tree (2s x s per node)
+  int s, D;
+  int cnt[9];         // item counts of levels l0 .. l0 + D
+  int nb[8];          // node bases of levels l0 .. l0 + D - 1
+  int identity_top;   // down: the top item is the identity (no M from above)
+};
+
+__global__ void __launch_bounds__(512) tsqr_up_group_kernel(const TreeGroupArgs a,
+                                                            const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  extern __shared__ double tsm[];
+  const int s = a.s, D = a.D, ss = s * s;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* b0 = tsm;
+  double* b1 = tsm + (size_t)(1 << D) * ss;
+  const int g = blockIdx.x;
+  const int lo = g << D, n0 = min(1 << D, a.cnt[0] - lo);
+  for (int e = threadIdx.x; e < n0 * ss; e += blockDim.x) b0[e] = a.in[(size_t)lo * ss + e];
+  __syncthreads();
+  for (int d = 0; d < D; ++d) {
+    const int lod = g << (D - d);
+    const int nd = min(1 << (D - d), a.cnt[d] - lod);
+    const int np = nd / 2;
+    for (int i = warp; i < np; i += nw)
+      warp_pair_qr(b0 + (size_t)2 * i * ss, b0 + (size_t)(2 * i + 1) * ss, s,
+                   a.nq + (size_t)(a.nb[d] + (lod >> 1) + i) * 2 * ss, b1 + (size_t)i * ss);
+    if (nd & 1)
+      for (int e = threadIdx.x; e < ss; e += blockDim.x) b1[(size_t)np * ss + e] = b0[(size_t)(nd - 1) * ss + e];
+    __syncthreads();
+    double* t = b0; b0 = b1; b1 = t;
+  }
+  for (int e = threadIdx.x; e < ss; e += blockDim.x) a.out[(size_t)g * ss + e] = b0[e];
+}
+
+__global__ void __launch_bounds__(512) tsqr_down_group_kernel(const TreeGroupArgs a,
+                                                              const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  extern __shared__ double tsm[];
+  const int s = a.s, D = a.D, ss = s * s;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* b0 = tsm;
+  double* b1 = tsm + (size_t)(1 << D) * ss;
+  const int g = blockIdx.x;
+  for (int e = threadIdx.x; e < ss; e += blockDim.x)
+    b0[e] = a.identity_top ? ((e % s) == (e / s) ? 1.0 : 0.0) : a.in[(size_t)g * ss + e];
+  __syncthreads();
+  for (int d = D - 1; d >= 0; --d) {
+    const int lod = g << (D - d);
+    const int nd = min(1 << (D - d), a.cnt[d] - lod);
+    const int np = nd / 2;
+    for (int i = warp; i < np; i += nw) {
+      const double* qn = a.nq + (size_t)(a.nb[d] + (lod >> 1) + i) * 2 * ss;
+      warp_mm(qn, 2 * s, b0 + (size_t)i * ss, s, b1 + (size_t)2 * i * ss);
+      warp_mm(qn + s, 2 * s, b0 + (size_t)i * ss, s, b1 + (size_t)(2 * i + 1) * ss);
+    }
+    if (nd & 1)
+      for (int e = threadIdx.x; e < ss; e += blockDim.x) b1[(size_t)(nd - 1) * ss + e] = b0[(size_t)np * ss + e];
+    __syncthreads();
+    double* t = b0; b0 = b1; b1 = t;
+  }
+  const int lo = g << D, n0 = min(1 << D, a.cnt[0] - lo);
+  for (int e = threadIdx.x; e < n0 * ss; e += blockDim.x) a.out[(size_t)lo * ss + e] = b0[e];
+}
+
+namespace {
+struct TreePlan {
+  int nlev = 0;
+  int cnt[40], nb[40];
+  std::vector<std::pair<int, int>> launches;  // (l0, D), bottom-up
+};
+TreePlan tree_plan(int L, int s) {
+  TreePlan t;
+  int c = L, base = 0;
+  while (true) {
+    t.cnt[t.nlev] = c;
+    t.nb[t.nlev] = base;
+    ++t.nlev;
+    if (c <= 1) break;
+    base += c / 2;
+    c = (c + 1) / 2;
+  }
+  const int dmax = s <= 8 ? 5 : 4;
+  for (int l0 = 0; l0 < t.nlev - 1;) {
+    const int D = std::min(dmax, t.nlev - 1 - l0);
+    t.launches.push_back({l0, D});
+    l0 += D;
+  }
+  return t;
+}
+TreeGroupArgs group_args(const TreePlan& t, int l0, int D, int s, double* nq) {
+  TreeGroupArgs a;
+  memset(&a, 0, sizeof a);
+  a.s = s;
+  a.D = D;
+  a.nq = nq;
+  for (int d = 0; d <= D; ++d) a.cnt[d] = t.cnt[l0 + d];
+  for (int d = 0; d < D; ++d) a.nb[d] = t.nb[l0 + d];
+  return a;
+}
+}  // namespace
+
+// Bottom-up tree of one shard's leaves [leaf_base, leaf_base + Lt) (leaf R's already in
+// the workspace); the shard root goes to root_out (s x s, ld s).
+cudaError_t tsqr_tree_up_shard(double* ws, int L, int leaf_base, int Lt, int s, double* root_out,
+                               const DevStatus* status, cudaStream_t st, int* launches) {
+  const size_t ss = (size_t)s * s;
+  double* R = ws + (size_t)leaf_base * ss;
+  double* Rt = ws + (size_t)L * ss + (size_t)leaf_base * ss;
+  double* nq = ws + (size_t)4 * L * ss + (size_t)leaf_base * 2 * ss;
+  if (Lt <= 1)
+    return cudaMemcpyAsync(root_out, R, ss * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  const TreePlan t = tree_plan(Lt, s);
+  double* bufs[2] = {R, Rt};
+  for (size_t j = 0; j < t.launches.size(); ++j) {
+    const int l0 = t.launches[j].first, D = t.launches[j].second;
+    TreeGroupArgs a = group_args(t, l0, D, s, nq);
+    a.in = bufs[j & 1];
+    a.out = j + 1 == t.launches.size() ? root_out : bufs[(j + 1) & 1];
+    const int groups = (t.cnt[l0] + (1 << D) - 1) >> D;
+    const size_t smem = (size_t)2 * (1 << D) * ss * sizeof(double);
+    cudaError_t e = ensure_smem(tsqr_up_group_kernel, smem);
+    if (e != cudaSuccess) return e;
+    tsqr_up_group_kernel<<<groups, 32 * std::max(1, (1 << D) / 2), smem, st>>>(a, status);
+    if (launches) *launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+// Top-down: the shard root's M (mtop, or identity when null) to the leaf M's in the
+// workspace's M region.
+cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s,
+                                 const double* mtop, const DevStatus* status, cudaStream_t st,
+                                 int* launches) {
+  const size_t ss = (size_t)s * s;
+  double* M = ws + (size_t)2 * L * ss + (size_t)leaf_base * ss;
+  double* Mt = ws + (size_t)3 * L * ss + (size_t)leaf_base * ss;
+  double* nq = ws + (size_t)4 * L * ss + (size_t)leaf_base * 2 * ss;
+  if (Lt <= 1) {
+    if (mtop) return cudaMemcpyAsync(M, mtop, ss * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    std::vector<double> id(ss, 0.0);
+    for (int i = 0; i < s; ++i) id[i + (size_t)i * s] = 1.0;
+    return cudaMemcpyAsync(M, id.data(), ss * sizeof(double), cudaMemcpyHostToDevice, st);
+  }
+  const TreePlan t = tree_plan(Lt, s);
+  const int K = (int)t.launches.size();
+  double* bufs[2] = {M, Mt};  // launch j writes level l0_j into bufs[j & 1] (j = 0 -> M)
+  for (int j = K - 1; j >= 0; --j) {
+    const int l0 = t.launches[j].first, D = t.launches[j].second;
+    TreeGroupArgs a = group_args(t, l0, D, s, nq);
+    a.out = bufs[j & 1];
+    if (j == K - 1) {
+      a.in = mtop;
+      a.identity_top = mtop ? 0 : 1;
+    } else {
+      a.in = bufs[(j + 1) & 1];
+    }
+    const int groups = (t.cnt[l0] + (1 << D) - 1) >> D;
+    const size_t smem = (size_t)2 * (1 << D) * ss * sizeof(double);
+    cudaError_t e = ensure_smem(tsqr_down_group_kernel, smem);
+    if (e != cudaSuccess) return e;
+    tsqr_down_group_kernel<<<groups, 32 * std::max(1, (1 << D) / 2), smem, st>>>(a, status);
+    if (launches) *launches += 1;
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------

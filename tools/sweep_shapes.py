@@ -33,8 +33,8 @@ def run(name, n, m, s):
 
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
-if which in ("all", "s"):
-    for s in (1, 2, 4, 8, 16):
+if which in ("all", "s", "s4"):
+    for s in ((4,) if which == "s4" else (1, 2, 4, 8, 16)):
         for name in NAMES:
             run(name, 1_000_000, 400, s)
 if which in ("all", "shape"):
