@@ -16,6 +16,7 @@
 // Every factor is carried as s x s (zero-padded rows for short leaves, which stack as
 // no-ops exactly like the reference's trapezoidal factors).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -191,6 +192,191 @@ __global__ void __launch_bounds__(kLeafThreads)
   }
   for (int j = 0; j < s; ++j)
     for (int i = tid; i < h; i += kLeafThreads) dst[g0 + i + (size_t)j * ldd] = sgn[j] * Q[i + j * h];
+}
+
+// ---------------------------------------------------------------------------------
+// Register-resident leaf Householder QR for s in {1, 2, 4, 8, 16}: thread t owns rows
+// t + 256 r (r < RPT) of the leaf; the reflector arithmetic is the generic kernel's
+// (scaled norm, alpha = -sign(a_kk) sigma, tau = 2 / v^T v, explicit Q by backward
+// accumulation, nonnegative-diagonal sign fix); only the row-to-thread assignment of the
+// partial sums differs.
+// ---------------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void cta_sum_t(double (&v)[NV], double* scratch /*[8][SMAX]*/,
+                                          double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const double r = warp_sum(v[i]);
+    if (lane == 0) scratch[warp * SMAX + i] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double acc = 0.0;
+    for (int w = 0; w < kLeafThreads / 32; ++w) acc += scratch[w * SMAX + threadIdx.x];
+    out[threadIdx.x] = acc;
+  }
+  __syncthreads();
+}
+
+template <int S, int RPT>
+__global__ void __launch_bounds__(kLeafThreads)
+    tsqr_leaf_reg_kernel(const double* __restrict__ src, long lds, double* __restrict__ dst,
+                         long ldd, const long* __restrict__ leaf_row0,
+                         double* __restrict__ rleaf, const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  __shared__ double scratch[8 * SMAX];
+  __shared__ double red[SMAX];
+  __shared__ double top[S];  // row k of the working matrix (A during the sweep, Q after)
+  __shared__ double v0s[S], taus[S], rdiag[S], rup[S * S];
+  const int tid = threadIdx.x;
+  const int l = blockIdx.x;
+  const long g0 = leaf_row0[l];
+  const int h = (int)(leaf_row0[l + 1] - g0);
+  const int p = h < S ? h : S;
+  double a[RPT][S];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = tid + r * kLeafThreads;
+#pragma unroll
+    for (int j = 0; j < S; ++j) a[r][j] = i < h ? src[g0 + i + (size_t)j * lds] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    if (k >= p) break;
+    // owner of row k publishes it (current values) for the top-row terms
+    if ((k & (kLeafThreads - 1)) == tid)
+#pragma unroll
+      for (int j = 0; j < S; ++j) top[j] = a[k / kLeafThreads][j];
+    double lm = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = tid + r * kLeafThreads;
+      if (i >= k && i < h) lm = fmax(lm, fabs(a[r][k]));
+    }
+    const double mx = cta_max(lm, scratch, red);  // (its barriers also publish top[])
+    if (mx == 0.0) {
+      if (tid == 0) { taus[k] = 0.0; v0s[k] = 0.0; rdiag[k] = top[k]; }
+      __syncthreads();
+      continue;
+    }
+    double v2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = tid + r * kLeafThreads;
+      if (i >= k && i < h) {
+        const double t = a[r][k] / mx;
+        v2[0] = fma(t, t, v2[0]);
+        if (i > k) v2[1] = fma(a[r][k], a[r][k], v2[1]);
+      }
+    }
+    cta_sum_t<2>(v2, scratch, red);
+    const double sigma = mx * sqrt(red[0]);
+    const double akk = top[k];
+    const double alpha = akk >= 0.0 ? -sigma : sigma;
+    const double v0 = akk - alpha;
+    const double vtv = v0 * v0 + red[1];
+    const double tau = vtv == 0.0 ? 0.0 : 2.0 / vtv;
+    __syncthreads();  // red[] is reused below
+    // w_j = tau (v0 a(k, j) + sum_{i > k} v_i a(i, j)), j > k
+    double w[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) w[j] = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = tid + r * kLeafThreads;
+      if (i > k && i < h)
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j > k) w[j] = fma(a[r][k], a[r][j], w[j]);
+    }
+    cta_sum_t<S>(w, scratch, red);
+#pragma unroll
+    for (int j = 0; j < S; ++j) w[j] = j > k ? tau * fma(v0, top[j], red[j]) : 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = tid + r * kLeafThreads;
+      if (i > k && i < h)
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j > k) a[r][j] -= w[j] * a[r][k];
+      if (i == k)
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j > k) a[r][j] -= w[j] * v0;
+    }
+    if (tid == 0) {
+      v0s[k] = v0;
+      taus[k] = tau;
+      rdiag[k] = alpha;
+    }
+    __syncthreads();
+  }
+  // R (before the sign fix): rows i < p of the swept matrix, diagonal = alpha
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = tid + r * kLeafThreads;
+    if (i < S)
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+        rup[i + j * S] = (i < p && i <= j) ? (i == j ? rdiag[i] : a[r][j]) : 0.0;
+  }
+  // Q = H_0 ... H_{p-1} [I; 0], accumulated backwards in registers
+  double q[RPT][S];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = tid + r * kLeafThreads;
+#pragma unroll
+    for (int j = 0; j < S; ++j) q[r][j] = (i == j && j < p) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = S - 1; k >= 0; --k) {
+    if (k >= p) continue;
+    const double tau = taus[k];
+    if (tau == 0.0) continue;
+    const double v0 = v0s[k];
+    if ((k & (kLeafThreads - 1)) == tid)
+#pragma unroll
+      for (int j = 0; j < S; ++j) top[j] = q[k / kLeafThreads][j];
+    double w[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) w[j] = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = tid + r * kLeafThreads;
+      if (i > k && i < h)
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+          if (j < p) w[j] = fma(a[r][k], q[r][j], w[j]);
+    }
+    cta_sum_t<S>(w, scratch, red);  // (its first barrier also publishes top[])
+#pragma unroll
+    for (int j = 0; j < S; ++j) w[j] = j < p ? tau * fma(v0, top[j], red[j]) : 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = tid + r * kLeafThreads;
+      if (i > k && i < h)
+#pragma unroll
+        for (int j = 0; j < S; ++j) q[r][j] -= w[j] * a[r][k];
+      if (i == k)
+#pragma unroll
+        for (int j = 0; j < S; ++j) q[r][j] -= w[j] * v0;
+    }
+    __syncthreads();
+  }
+  // canonical sign: nonnegative diag(R)
+  double sg[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) sg[j] = (j < p && rup[j + j * S] < 0.0) ? -1.0 : 1.0;
+  if (tid < S * S) rleaf[(size_t)l * S * S + tid] = sg[tid % S] * rup[tid];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = tid + r * kLeafThreads;
+    if (i < h)
+#pragma unroll
+      for (int j = 0; j < S; ++j) dst[g0 + i + (size_t)j * ldd] = sg[j] * q[r][j];
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -579,6 +765,23 @@ size_t tsqr_ws_bytes(int leaves, int s) {
 cudaError_t tsqr_leaf_launch(const double* src, long lds, double* dst, long ldd,
                              const long* d_bounds, int L, long hmax, int s, double* rleaf,
                              const DevStatus* status, cudaStream_t st, int* launches) {
+  static const bool generic = [] {
+    const char* e = getenv("BGS_TSQR_GENERIC");
+    return e && *e && *e != '0';
+  }();
+#define BGS_LEAF_REG(S_, RPT_)                                                             \
+  if (!generic && s == S_ && hmax <= (long)RPT_ * kLeafThreads) {                                     \
+    tsqr_leaf_reg_kernel<S_, RPT_><<<L, kLeafThreads, 0, st>>>(src, lds, dst, ldd, d_bounds, \
+                                                              rleaf, status);              \
+    if (launches) *launches += 1;                                                          \
+    return cudaGetLastError();                                                             \
+  }
+  BGS_LEAF_REG(1, 4)
+  BGS_LEAF_REG(2, 4)
+  BGS_LEAF_REG(4, 4)
+  BGS_LEAF_REG(8, 2)
+  BGS_LEAF_REG(16, 1)
+#undef BGS_LEAF_REG
   const size_t smem = (size_t)2 * (hmax > 0 ? hmax : 1) * s * sizeof(double);
   cudaError_t e = ensure_smem(tsqr_leaf_kernel, smem);
   if (e != cudaSuccess) return e;
