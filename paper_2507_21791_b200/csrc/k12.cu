@@ -31,7 +31,7 @@
 //   epilogue on the tensor core: [A | B] = [srcA - DA | srcB - DB] M, M = [[TA^-1,
 //            -TA^-1 W], [0, TB^-1]], W = S2 TB^-1 (2 DMMAs per 8 rows).
 //   Gram     this rank's output tiles (warp w: tiles w + 4jj) against span 1, DMMA.8x8x4,
-//            folded into double-double (hi, lo) after every stage.
+//            folded into double-double (hi, lo) every 4 group-stages.
 // Output tiles: rank 0 = own span-0 units + the span-1 left units, rank 1 = its own span-0
 // units.  The two groups' double-doubles are combined in the CTA at the end; one partial
 // slot per cluster (every tile written by exactly one rank) -> gram_reduce.
@@ -267,11 +267,27 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       acol[jj] = 8 * lu + ii;
     }
 
-    double hi[MTW][2], lo[MTW][2];
+    // (hi, lo) double-double per output; the stage contractions accumulate in acc and are
+    // folded in every kFold group-stages (<= 4 x 128 rows of plain fp64 per fold; folding
+    // every stage costs ~7% of the kernel: the two_sums share the FP64 pipe with DMMA)
+    constexpr int kFold = 4;
+    double hi[MTW][2], lo[MTW][2], acc[MTW][2];
 #pragma unroll
     for (int j = 0; j < MTW; ++j)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) hi[j][e] = lo[j][e] = 0.0;
+      for (int e = 0; e < 2; ++e) hi[j][e] = lo[j][e] = acc[j][e] = 0.0;
+    auto fold = [&]() {
+#pragma unroll
+      for (int jj = 0; jj < MTW; ++jj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double sm, err;
+          two_sum(hi[jj][e], acc[jj][e], sm, err);
+          hi[jj][e] = sm;
+          lo[jj][e] += err;
+          acc[jj][e] = 0.0;
+        }
+    };
 
     const uint32_t sbase = smem_u32(smem);
     const uint32_t red_g = smem_u32(redbuf) + (uint32_t)(g * kGroupWarps * 4 * 32 * 16);
@@ -409,9 +425,6 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       if (prof) { const unsigned long long t = clock64(); ph[3] += t - t1; t1 = t; }
 
       // ---- Gram of this rank's output tiles (w + 4 jj) against span 1 ----
-      double acc[MTW][2];
-#pragma unroll
-      for (int jj = 0; jj < MTW; ++jj) acc[jj][0] = acc[jj][1] = 0.0;
       // k-index kk of pass u covers chunk rows 16 (kk & 1) + 8 (kk >> 1) + 4u + {0..3}: for
       // the two tile columns of a quarter-warp the chunk sets are S and S ^ 2 with
       // S = {0, 1, 4, 5} (u = 0) or {2, 3, 6, 7} (u = 1) -> conflict-free, no swap.
@@ -448,17 +461,10 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       fence_proxy_async();  // generic writes of A / B before TMA refills the slot
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
-#pragma unroll
-      for (int jj = 0; jj < MTW; ++jj)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double sm, err;
-          two_sum(hi[jj][e], acc[jj][e], sm, err);
-          hi[jj][e] = sm;
-          lo[jj][e] += err;
-        }
+      if ((j % kFold) == kFold - 1) fold();
       if (prof) { const unsigned long long t = clock64(); ph[4] += t - t1; }
     }
+    fold();
     if (prof) {
       ph[5] = clock64() - t_begin;
       unsigned long long* dst = p.phase + (size_t)blockIdx.x * 16 + 8 * g;
