@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     // (hi, lo) double-double per output; the stage contractions accumulate in acc and are
     // folded in every kFold group-stages (<= 4 x 128 rows of plain fp64 per fold; folding
     // every stage costs ~7% of the kernel: the two_sums share the FP64 pipe with DMMA)
-    constexpr int kFold = 4;
+    constexpr int kFold = MTW >= 9 ? 1 : 4;  // (MTW = 9: registers for acc are short)
     double hi[MTW][2], lo[MTW][2], acc[MTW][2];
 #pragma unroll
     for (int j = 0; j < MTW; ++j)
@@ -562,8 +562,7 @@ bool k12_plan(SplitParams& p) {
     const int KS = 4 / cd.R;
     const int kw = (std::max(k0, k1) + KS - 1) / KS;
     const int mtw = (std::max(mt0, mt1) + kGroupWarps - 1) / kGroupWarps;
-    // (KW = 16 with R = 1 needs MTW = 9 and spills; that shape goes to the pair instead)
-    const int kw_max = cd.R == 1 ? 14 : kKwMax;
+    const int kw_max = kKwMax;
     int kw_t = std::max(2, (kw + 1) / 2 * 2);
     while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) kw_t += 2;
     if (kw_t > kw_max) continue;
@@ -617,9 +616,7 @@ static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
     case 10: return launch_k12<10, R>(p, grid, st);
     case 12: return launch_k12<12, R>(p, grid, st);
     case 14: return launch_k12<14, R>(p, grid, st);
-    case 16:
-      if (R == 1) return cudaErrorInvalidValue;  // not planned (spills)
-      return launch_k12<16, R == 1 ? 2 : R>(p, grid, st);
+    case 16: return launch_k12<16, R>(p, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
