@@ -213,7 +213,9 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     const int qd = w % R, kpart = w / R;
     const int pc1 = min(8 * (own_u0 + own_n), p.kp);
     const int kcols = max(0, pc1 - 8 * own_u0);
-    const int ksteps = kcols / 4;  // whole k-steps (k12_plan)
+    // The last k-step may be partial (s = 1, 2, 3): its columns past kcols have zero
+    // coefficients and hold finite data (the A block, or Q columns zeroed by the runtime).
+    const int ksteps = (kcols + 3) / 4;
     const int jlast = max(ksteps - 1, 0);
     double bco[KW];
 #pragma unroll
@@ -542,8 +544,7 @@ bool k12_plan(SplitParams& p) {
       q.own_u0[0] = 0; q.own_n[0] = p.U0; q.ext_u0[0] = 0; q.ext_n[0] = 0;
       q.own_u0[1] = q.own_n[1] = q.ext_u0[1] = q.ext_n[1] = 0;
       q.slot_units = p.U0 + p.U1;
-      if (p.kp % 4) continue;
-      k0 = p.kp / 4;
+      k0 = (p.kp + 3) / 4;
       mt0 = p.U0 + q.s1_left;
     } else {
       const int uh = (p.U0 - na + 1) / 2;
@@ -553,9 +554,8 @@ bool k12_plan(SplitParams& p) {
       q.ext_u0[1] = 0;         q.ext_n[1] = 0;
       q.slot_units = std::max(uh + na, p.U0 - uh) + p.U1;
       const int c0 = std::min(8 * uh, p.kp), c1 = std::max(0, p.kp - 8 * uh);
-      if (c0 % 4 || c1 % 4) continue;  // whole k-steps only (always true for s = 4)
-      k0 = c0 / 4;
-      k1 = c1 / 4;
+      k0 = (c0 + 3) / 4;
+      k1 = (c1 + 3) / 4;
       mt0 = uh + q.s1_left;
       mt1 = p.U0 - uh;
     }

@@ -1599,6 +1599,11 @@ int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0
     run.sh.push_back(sh);
     c->launches = 0;
     CUDA_OK(cudaEventRecord(c->e0, c->stream));
+    // For s not a multiple of 4 the fused kernel's last k-step reads a few Q columns that
+    // are not computed yet (zero coefficients): they must hold finite values.
+    if (s % 4 && n_local > 0)
+      CUDA_OK(cudaMemset2DAsync(d_q, ldq * sizeof(double), 0, n_local * sizeof(double), m,
+                                c->stream));
     run.run();
     CUDA_OK(cudaEventRecord(c->e1, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
