@@ -345,3 +345,22 @@ def test_chunked_gram_matches_oracle(oracle, gpu_ctx, monkeypatch):
     assert out.ok and out.stats.event_labels == ref.labels
     assert_r_close(out.r, ref.r)
     assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
+
+
+@pytest.mark.parametrize("s", [2, 3, 4])
+def test_factor_device_ignores_stale_q(gpu_ctx, s):
+    """bgs_factor_device on a caller's Q buffer full of NaN: no uncomputed Q column may leak
+    into the result (s % 4 != 0 reads a few of them with zero coefficients)."""
+    import torch
+    import paper_2507_21791_b200 as bgs
+    n, m = 50007, 96 if s != 3 else 93
+    ld = (n + 31) // 32 * 32
+    x = bgs.gen_gaussian_host(31337, n, m)
+    X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    X[:, :n] = torch.from_numpy(np.asfortranarray(x).T.copy()).cuda()
+    Q = torch.full((m, ld), float("nan"), dtype=torch.float64, device="cuda")
+    r, st, tm = bgs.factor_device(gpu_ctx, 3, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+    q = Q[:, :n].cpu().numpy().T
+    assert np.isfinite(q).all() and np.isfinite(r).all()
+    ref = bgs.run_factor(3, x, s, 1, metrics=False, ctx=gpu_ctx)
+    assert np.abs(r - ref.r).max() <= 1e-12 * np.abs(ref.r).max()
