@@ -37,32 +37,59 @@ def parse():
     ap.add_argument("--m", type=int, default=400)
     ap.add_argument("--s", type=int, default=4)
     ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--dist", default="gaussian", choices=["gaussian", "geometric"],
+                    help="i.i.d. N(0,1) (configs 1-4) or U diag(sigma) V^T (config 5)")
+    ap.add_argument("--kappa", type=float, default=1e6, help="geometric: cond(X)")
+    ap.add_argument("--config", type=int, default=0, choices=[0, 1, 2, 5],
+                    help="BASELINE.json preset: 1 (n=1e5 m=64), 2 (n=1e6 m=400, the default "
+                         "workload), 5 (n=1e7 m=400 geometric kappa=1e6)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU seconds of one reference sample run")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.config == 1:
+        a.n, a.m, a.s, a.dist = 100_000, 64, 4, "gaussian"
+    elif a.config == 2:
+        a.n, a.m, a.s, a.dist = 1_000_000, 400, 4, "gaussian"
+    elif a.config == 5:
+        a.n, a.m, a.s, a.dist, a.kappa = 10_000_000, 400, 4, "geometric", 1e6
+    return a
+
+
+def config_id(a):
+    for cid, (n, m, s, dist) in {1: (100_000, 64, 4, "gaussian"), 2: (1_000_000, 400, 4, "gaussian"),
+                                 5: (10_000_000, 400, 4, "geometric")}.items():
+        if (a.n, a.m, a.s, a.dist) == (n, m, s, dist) and (dist == "gaussian" or a.kappa == 1e6):
+            return f"BASELINE.json config {cid}"
+    return "custom shape"
+
+
+def dist_text(a):
+    return ("i.i.d. N(0,1)" if a.dist == "gaussian"
+            else f"U diag(sigma) V^T, sigma log-spaced 1..{1 / a.kappa:g}")
 
 
 def workload_config(a, world):
     return {
-        "workload": f"{a.variant} n={a.n} m={a.m} s={a.s} fp64 i.i.d. N(0,1) "
-                    f"(BASELINE.json config 2)",
+        "workload": f"{a.variant} n={a.n} m={a.m} s={a.s} fp64 {dist_text(a)} ({config_id(a)})",
         "variant": a.variant, "n": a.n, "m": a.m, "s": a.s, "seed": a.seed,
+        "dist": a.dist, **({"kappa": a.kappa} if a.dist == "geometric" else {}),
         "parallelism": f"row-sharded dp{world} (1-D ceil split), 1 allreduce per block step",
         "l2": f"inputs exceed L2: X is {a.n * a.m * 8 / 1e9:.2f} GB (126 MB L2), no flush needed",
     }
 
 
 def metric_name(a):
-    return f"fp64 QR time & GFLOP/s, {a.variant} n={a.n:.0e} m={a.m} s={a.s}".replace("+0", "")
+    geo = "" if a.dist == "gaussian" else f" geometric kappa={a.kappa:.0e}".replace("+0", "")
+    return f"fp64 QR time & GFLOP/s, {a.variant} n={a.n:.0e} m={a.m} s={a.s}{geo}".replace("+0", "")
 
 
 # ---------------------------------------------------------------------------------------
 # CPU reference (test-infrastructure checker, timed on the host cores)
 # ---------------------------------------------------------------------------------------
-def cpu_reference_runner(v, n, m, s, seed):
+def cpu_reference_runner(v, n, m, s, seed, gaussian=True, kappa=1.0):
     """Returns (kind, run(n_rows) -> (seconds, flops))."""
     from oracle.oracle import Oracle, Reference
     cores = os.cpu_count() or 1
@@ -71,7 +98,7 @@ def cpu_reference_runner(v, n, m, s, seed):
         kind = "reference"
 
         def run(rows):
-            x = ref.gen_matrix(rows, m, s, 1.0, seed, True)
+            x = ref.gen_matrix(rows, m, s, kappa if not gaussian else 1.0, seed, gaussian)
             res = ref.factor(v, x, s, procs=cores, want_q=False)
             return res.seconds
     else:
@@ -80,7 +107,7 @@ def cpu_reference_runner(v, n, m, s, seed):
         cores = int(os.environ.get("OMP_NUM_THREADS", cores))
 
         def run(rows):
-            x = ref.gen_matrix(rows, m, s, 1.0, seed, True)
+            x = ref.gen_matrix(rows, m, s, kappa if not gaussian else 1.0, seed, gaussian)
             t = time.perf_counter()
             ref.factor(v, x, s, 1)
             return time.perf_counter() - t
@@ -180,7 +207,8 @@ def run_reference_arm(a):
     import paper_2507_21791_b200 as bgs
     v = bgs.parse_variant(a.variant)
     per_step = max(2.0, a.cpu_seconds * 8.0 / max(8, a.steps + a.warmup))
-    kind, cores, run = cpu_reference_runner(int(v), a.n, a.m, a.s, a.seed)
+    kind, cores, run = cpu_reference_runner(int(v), a.n, a.m, a.s, a.seed, a.dist == "gaussian",
+                                            a.kappa)
     rows, _ = pick_sample_rows(run, a.n, a.m, per_step)
     for _ in range(a.warmup):
         run(rows)
@@ -188,14 +216,15 @@ def run_reference_arm(a):
     t = sum(secs) / len(secs)
     flops = bgs.variant_flops(int(v), rows, a.m, a.s)
     gf = flops / t / 1e9
-    sample = (f"{a.variant} n={rows} m={a.m} s={a.s} N(0,1) (row subsample of the workload; "
+    sample = (f"{a.variant} n={rows} m={a.m} s={a.s} {dist_text(a)} (row subsample of the workload; "
               f"cost and flops both scale with n), {'reference library oracle/_ref' if kind == 'reference' else 'oracle port'} "
               f"run_variant under run_spmd with P={cores} threads, mean of {a.steps} runs")
     line = {
         "impl": "reference", "metric": metric_name(a), "value": gf, "unit": "GFLOP/s",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": t * 1e3 * (a.n / rows), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), reference gen_matrix)",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded {dist_text(a)}, reference gen_matrix)",
         "config": workload_config(a, world),
         "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": kind,
                          "sample": sample},
@@ -247,7 +276,12 @@ def run_ours(a):
     ld = max(32, (nl + 31) // 32 * 32)  # tile engine reads whole 16-row blocks (bgs_gpu.h)
     X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
     Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
-    bgs.gen_gaussian_device(ctx, a.seed, row0, nl, m, X.data_ptr(), ld)
+    if a.dist == "gaussian":
+        bgs.gen_gaussian_device(ctx, a.seed, row0, nl, m, X.data_ptr(), ld)
+    else:  # config 5: U diag(sigma) V^T built on the GPUs (paper_2507_21791_b200/matgen.py)
+        from paper_2507_21791_b200 import matgen
+        matgen.geometric_device(ctx, n, m, a.kappa, a.seed, row0, nl, X, ld, scratch=Q)
+        Q.zero_()
     torch.cuda.synchronize()
     flops = bgs.variant_flops(v, n, m, s)
 
@@ -358,12 +392,13 @@ def run_ours(a):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         try:
-            kind, cores, run = cpu_reference_runner(v, n, m, s, a.seed)
+            kind, cores, run = cpu_reference_runner(v, n, m, s, a.seed, a.dist == "gaussian",
+                                                    a.kappa)
             rows, _ = pick_sample_rows(run, n, m, a.cpu_seconds)
             t = run(rows)
             gf = bgs.variant_flops(v, rows, m, s) / t / 1e9
             cpu = {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": kind,
-                   "sample": f"{a.variant} n={rows} m={m} s={s} N(0,1) (row subsample; cost and "
+                   "sample": f"{a.variant} n={rows} m={m} s={s} {dist_text(a)} (row subsample; cost and "
                              f"flops both linear in n), {t:.1f} s, run_variant under run_spmd "
                              f"with P={cores} threads",
                    "extrapolated_ms_full_n": t * 1e3 * n / rows}
@@ -377,7 +412,9 @@ def run_ours(a):
             "metric": metric_name(a), "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded i.i.d. N(0,1) generated on device (Philox)",
+            "data": ("synthetic: seeded i.i.d. N(0,1) generated on device (Philox)" if a.dist == "gaussian"
+                     else "synthetic: X = U diag(sigma) V^T generated on device (U = QR of a Philox "
+                          "Gaussian by this library, V host Haar, DGEMM)"),
             "config": workload_config(a, world),
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"],
                        "reasons": clocks["reasons"], "samples": clocks["samples"]},

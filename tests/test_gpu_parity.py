@@ -364,3 +364,30 @@ def test_factor_device_ignores_stale_q(gpu_ctx, s):
     assert np.isfinite(q).all() and np.isfinite(r).all()
     ref = bgs.run_factor(3, x, s, 1, metrics=False, ctx=gpu_ctx)
     assert np.abs(r - ref.r).max() <= 1e-12 * np.abs(ref.r).max()
+
+
+def test_geometric_kappa_1e6_matches_oracle(oracle, gpu_ctx):
+    """Config 5's matrix family (X = U diag(sigma) V^T, sigma log-spaced 1..1e-6) at reduced
+    size on the oracle's own bits: the orthogonality loss tracks the reference's."""
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 100_000, 64, 4
+    x = oracle.gen_matrix(n, m, s, 1e6, 12345, False)
+    ref = oracle.factor(3, x, s, 1, metrics=True)
+    out = bgs.run_factor(3, x, s, 1, metrics=False)
+    assert out.ok and out.stats.event_labels == ref.labels
+    assert_structure(out.r)
+    assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
+    assert oracle.residual(x, out.q, out.r) <= 10 * max(ref.resid, U)
+
+
+def test_gpu_geometric_generator(gpu_ctx):
+    """matgen.geometric_device: X = U diag(sigma) V^T with orthonormal U, V: the singular
+    values of the generated matrix are the schedule."""
+    import torch
+    from paper_2507_21791_b200 import matgen
+    n, m = 20000, 48
+    ld = (n + 31) // 32 * 32
+    X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
+    matgen.geometric_device(gpu_ctx, n, m, 1e4, 7, 0, n, X, ld)
+    sv = np.linalg.svd(X[:, :n].cpu().numpy().T, compute_uv=False)
+    assert np.allclose(sv, matgen.sigma_schedule(m, 1e4), rtol=1e-10, atol=0)
