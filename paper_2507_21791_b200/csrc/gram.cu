@@ -31,6 +31,7 @@
 //     a k-step sit on lines with distinct (L & 7), so 16 lanes hit 16 distinct slots.
 #include "common.cuh"
 #include "kernels.h"
+#include "reduce.cuh"
 
 namespace bgs {
 
@@ -443,67 +444,9 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant
   }
 }
 
-// Deterministic cross-CTA reduction in double-double, rank-local.  A CTA handles 16
-// output entries with 16 slices each: slice l sums partials g = l, l+16, ... in order
-// (8 independent loads in flight per thread), then the 16 slice sums are combined in
-// slice order.  Fixed order -> reproducible.
-constexpr int RED_ENTRIES = 16, RED_SLICES = 16, RED_BATCH = 8;
-__global__ void __launch_bounds__(RED_ENTRIES * RED_SLICES)
-    gram_reduce_kernel(const double2* __restrict__ part, int G, int mt_out, int N8, int N,
-                       int ubox0, int lcols0, int lcols1, int M, double* __restrict__ out,
-                       const DevStatus* status) {
-  // (no status check: after a failure the next small op returns first, and skipping
-  // it here saves a dependent global load in front of the partial loads)
-  (void)status;
-  __shared__ double2 red[RED_SLICES][RED_ENTRIES];
-  const int le = threadIdx.x % RED_ENTRIES, sl = threadIdx.x / RED_ENTRIES;
-  const int idx = blockIdx.x * RED_ENTRIES + le;
-  const int per_cta = mt_out * 8 * N8;
-  double s = 0.0, e = 0.0;
-  if (idx < per_cta) {
-    const double2* ptr = part + idx;
-    for (int g0 = sl; g0 < G; g0 += RED_SLICES * RED_BATCH) {
-      double2 v[RED_BATCH];
-#pragma unroll
-      for (int u = 0; u < RED_BATCH; ++u) {
-        const int g = g0 + u * RED_SLICES;
-        v[u] = g < G ? __ldg(ptr + (size_t)g * per_cta) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < RED_BATCH; ++u) {  // adding (0, 0) leaves (s, e) unchanged
-        double s2, err;
-        two_sum(s, v[u].x, s2, err);
-        s = s2;
-        e += err + v[u].y;
-      }
-    }
-  }
-  red[sl][le] = make_double2(s, e);
-  __syncthreads();
-  if (sl != 0 || idx >= per_cta) return;
-  s = 0.0;
-  e = 0.0;
-  for (int l = 0; l < RED_SLICES; ++l) {
-    const double2 v = red[l][le];
-    double s2, err;
-    two_sum(s, v.x, s2, err);
-    s = s2;
-    e += err + v.y;
-  }
-  const int n = idx % N8;
-  const int i = (idx / N8) % 8;
-  const int t = idx / (8 * N8);
-  if (n >= N) return;
-  int row;
-  if (t < ubox0) {
-    row = 8 * t + i;
-    if (row >= lcols0) return;
-  } else {
-    const int r = 8 * (t - ubox0) + i;
-    if (r >= lcols1) return;
-    row = lcols0 + r;
-  }
-  out[row + (size_t)n * M] = s + e;
+// Deterministic cross-CTA reduction in double-double, rank-local (reduce.cuh).
+__global__ void __launch_bounds__(RED_THREADS) gram_reduce_kernel(const ReduceArgs a) {
+  gram_reduce_body(a);
 }
 
 // ------------------------------------------------------------------------------------
@@ -612,15 +555,33 @@ cudaError_t tile_launch(TileParams& p, bool upd, int grid, cudaStream_t st, int*
   }
 }
 
+ReduceArgs reduce_args(const TileParams& p, int ctas, double* out, int ld_out) {
+  ReduceArgs a;
+  a.part = reinterpret_cast<const double2*>(p.partial);
+  a.G = ctas;
+  a.mt_out = p.mt_out;
+  a.N8 = 8 * gram_n_tiles(p.N);
+  a.N = p.N;
+  a.ubox0 = p.units_span[0];
+  a.lcols0 = p.lcols[0];
+  a.lcols1 = p.mt_out > p.units_span[0] ? p.lcols[1] : 0;
+  a.M = ld_out > 0 ? ld_out : a.lcols0 + a.lcols1;
+  a.out = out;
+  return a;
+}
+
+cudaError_t gram_reduce_launch_args(const ReduceArgs& a, int entries, cudaStream_t st,
+                                    int* launches) {
+  gram_reduce_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, RED_THREADS, 0, st>>>(a);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t gram_reduce_launch(const TileParams& p, int ctas, double* out, cudaStream_t st,
                                int* launches, int ld_out) {
-  const int N8 = 8 * gram_n_tiles(p.N);
-  const int entries = p.mt_out * 8 * N8;
-  const int lc1 = p.mt_out > p.units_span[0] ? p.lcols[1] : 0;
-  gram_reduce_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, RED_ENTRIES * RED_SLICES, 0,
-                       st>>>(reinterpret_cast<const double2*>(p.partial), ctas, p.mt_out, N8, p.N,
-                             p.units_span[0], p.lcols[0], lc1,
-                             ld_out > 0 ? ld_out : p.lcols[0] + lc1, out, p.status);
+  const int entries = p.mt_out * 8 * 8 * gram_n_tiles(p.N);
+  gram_reduce_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, RED_THREADS, 0, st>>>(
+      reduce_args(p, ctas, out, ld_out));
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

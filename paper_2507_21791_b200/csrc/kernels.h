@@ -155,6 +155,15 @@ struct SmallParams {
   DevStatus* status;
 };
 cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches);
+// gram_reduce followed by the s <= 4 one-sync step in one launch (single-GPU contexts: the
+// step needs the fully reduced Gram, so no allreduce may sit in between).
+struct ReduceArgs;
+ReduceArgs reduce_args(const TileParams& p, int ctas, double* out, int ld_out);
+bool small_mergeable(const SmallParams& p);
+cudaError_t gram_reduce_launch_args(const ReduceArgs& a, int entries, cudaStream_t st,
+                                    int* launches);
+cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallParams& p,
+                                unsigned* ticket, cudaStream_t st, int* launches);
 
 // ---------------- K4: TSQR (tsqr.cu) ----------------
 // Workspace for a TSQR over L leaves of width s: regions [R | Rtmp | M | Mtmp] of

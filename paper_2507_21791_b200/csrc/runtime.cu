@@ -31,6 +31,7 @@
 #include "../../include/bgs_gpu.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "reduce.cuh"
 
 using namespace bgs;
 
@@ -208,6 +209,7 @@ struct bgs_ctx {
   DBuf tsqr_ws, tsqr_bounds, tsqr_trees, roots, roots_all, cross_ws, cross_m, metrics;
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
   std::vector<DBuf> rscr;    // per-shard right-operand scratch of chunked Grams
+  DBuf ticket;               // last-CTA ticket of the merged reduce + step kernel
   int launches = 0;
   // live profiler: event pairs per launch, resolved after the stream syncs
   struct ProfClass {
@@ -256,6 +258,7 @@ struct bgs_ctx {
       b->release();
     for (auto& b : sx) b.release();
     for (auto& b : rscr) b.release();
+    ticket.release();
     for (auto& b : sq) b.release();
     for (auto& p : pending) {
       event_pool.push_back(p.a);
@@ -335,6 +338,7 @@ class Runner {
   bool no_k12c = false;
   bool prof_step = false;  // BGS_PROF_STEP: one profiler class per fused block step
   int gram_max_units = 0;  // BGS_GRAM_MAXUNITS (tests): chunk unfused Grams above this
+  bool no_merge_small = false;  // BGS_NO_MERGE_SMALL: separate reduce and small launches
   int tile_dbg = 0;
   bool tile_prof = false;
 
@@ -349,6 +353,8 @@ class Runner {
     prof_step = e3 && *e3 && *e3 != '0';
     const char* e4 = getenv("BGS_GRAM_MAXUNITS");
     gram_max_units = e4 ? atoi(e4) : 0;
+    const char* e5 = getenv("BGS_NO_MERGE_SMALL");
+    no_merge_small = e5 && *e5 && *e5 != '0';
     const char* d = getenv("BGS_TILE_DBG");
     tile_dbg = d ? atoi(d) : 0;
     const char* tp = getenv("BGS_TILE_PROF");
@@ -421,6 +427,8 @@ class Runner {
     c->status.ensure(sizeof(DevStatus));
     status = reinterpret_cast<DevStatus*>(c->status.p);
     CUDA_OK(cudaMemsetAsync(status, 0, sizeof(DevStatus), c->stream));
+    c->ticket.ensure(64);
+    CUDA_OK(cudaMemsetAsync(c->ticket.p, 0, 64, c->stream));
     c->R.ensure((size_t)m * m * sizeof(double));
     CUDA_OK(cudaMemsetAsync(c->R.p, 0, (size_t)m * m * sizeof(double), c->stream));
     const long Mmax = m + 2 * s + 16;
@@ -574,10 +582,7 @@ class Runner {
     rp.lcols[0] = lc[0];
     rp.lcols[1] = lc[1];
     rp.status = status;
-    {
-      Prof pr(c, "gram_reduce", (double)slot_base * per_slot * 8.0, 0.0);
-      CUDA_OK(gram_reduce_launch(rp, slot_base, c->G.d(), c->stream, &c->launches));
-    }
+    reduce(rp, slot_base, c->G.d(), 0, (double)slot_base * per_slot * 8.0);
     if (use_nccl && do_allreduce) {
       Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
       NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
@@ -585,6 +590,36 @@ class Runner {
     }
     if (count_sync) record(label, (long)M * p.N);
     return M;
+  }
+
+  // A Gram reduction held back so the one-sync step's small op can run in the same launch
+  // (reduce_step4_kernel).  Only inside onesync(), only on single-GPU contexts (no
+  // allreduce may sit between the two); every other launch flushes it first.
+  struct PendingReduce {
+    bool on = false;
+    ReduceArgs a;
+    int entries = 0;
+    double bytes = 0.0;
+  };
+  PendingReduce pend;
+  bool defer_reduce = false;
+  void flush_reduce() {
+    if (!pend.on) return;
+    pend.on = false;
+    Prof pr(c, "gram_reduce", pend.bytes, 0.0);
+    CUDA_OK(gram_reduce_launch_args(pend.a, pend.entries, c->stream, &c->launches));
+  }
+  // launch (or hold back) the reduction of `slots` partial slots described by rp
+  void reduce(const TileParams& rp, int slots, double* out, int ld_out, double bytes) {
+    if (defer_reduce && !use_nccl && !gout) {
+      pend.on = true;
+      pend.a = reduce_args(rp, slots, out, ld_out);
+      pend.entries = rp.mt_out * 8 * 8 * gram_n_tiles(rp.N);
+      pend.bytes = bytes;
+      return;
+    }
+    Prof pr(c, "gram_reduce", bytes, 0.0);
+    CUDA_OK(gram_reduce_launch(rp, slots, out, c->stream, &c->launches, ld_out));
   }
 
   static const CUtensorMap& map_of(const Shard& x, int src, int hi, int wi) {
@@ -656,6 +691,7 @@ class Runner {
   // Returns M (rows of the compact Gram written to c->G, ld = M).
   int gram(const GramSpec& sp, const char* label, bool count_sync = true,
            bool do_allreduce = true, const Fuse* fz = nullptr) {
+    flush_reduce();
     for (int i = 0; i < sp.nspans; ++i)
       if (sp.sp[i].src == SX) need_x(sp.sp[i].col0 + sp.sp[i].ncols);
     TileParams p;
@@ -755,11 +791,7 @@ class Runner {
       cta_base += grid;
     }
     p.partial = c->partial.d();
-    {
-      Prof pr(c, "gram_reduce", (double)cta_base * per_cta * 8.0, 0.0);
-      CUDA_OK(gram_reduce_launch(p, cta_base, gout ? gout : c->G.d(), c->stream, &c->launches,
-                                 gout ? gout_ld : 0));
-    }
+    reduce(p, cta_base, gout ? gout : c->G.d(), gout ? gout_ld : 0, (double)cta_base * per_cta * 8.0);
     if (use_nccl && do_allreduce) {
       Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
       NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
@@ -779,6 +811,7 @@ class Runner {
     const double* CB = nullptr; long ldcb = 0; const double* TB = nullptr;
   };
   void update(const Upd& u) {
+    flush_reduce();
     if (u.has_a && u.srcA == SX) need_x(u.colA + s);
     if (u.has_b && u.srcB == SX) need_x(u.colB + s);
     for (auto& x : sh) {
@@ -821,6 +854,14 @@ class Runner {
     p.R = c->R.d();
     p.ldr = (int)m;
     p.status = status;
+    if (pend.on && small_mergeable(p)) {
+      pend.on = false;
+      Prof pr(c, "reduce_small", pend.bytes, 0.0);
+      CUDA_OK(reduce_small_launch(pend.a, pend.entries, p, static_cast<unsigned*>(c->ticket.p),
+                                  c->stream, &c->launches));
+      return;
+    }
+    flush_reduce();
     Prof pr(c, "small", 0.0, 0.0);
     CUDA_OK(small_launch(p, c->stream, &c->launches));
   }
@@ -830,6 +871,7 @@ class Runner {
   // rendezvous (tsqr_fused_gram, intraorth.cpp:122-135).
   void tsqr(int src, long scol_, long dcol, double* rout, int ldrout, const char* label,
             long fused_words = 0, double* fusedG = nullptr) {
+    flush_reduce();
     if (src == SX) need_x(scol_ + s);
     const size_t ss = (size_t)s * s;
     double* ws = c->tsqr_ws.d();
@@ -947,6 +989,11 @@ class Runner {
   // onesync_impl (bcgs.cpp:233-369); modes PythChol (P-1S), SkipNorm (I+1S), TsqrPath (P-2S)
   void onesync(int mode, int kappa_power) {
     if (q == 1) return single_block();
+    defer_reduce = !no_merge_small;
+    struct Undefer {
+      Runner* r;
+      ~Undefer() { r->defer_reduce = false; }
+    } undefer{this};
     const int si = (int)s;
     double* scol_cur = c->scolA.d();
     double* scol_nxt = c->scolB.d();
@@ -1217,6 +1264,7 @@ class Runner {
       case BGS_BCGSI_PLUS_1S: onesync(OS_SKIP, 3); break;
       default: fail(BGS_E_CONFIG, "variant %d is out of scope", variant);
     }
+    flush_reduce();
     q_final(m);
   }
 

@@ -13,6 +13,7 @@
 // device buffers read by K2; the host never waits on them.
 #include "common.cuh"
 #include "kernels.h"
+#include "reduce.cuh"
 
 namespace bgs {
 
@@ -376,7 +377,7 @@ BGS_DEV int trsm4(const double (&g)[16], const double (&b)[16], int s, double (&
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kStepThreads, 1) onesync_step4_kernel(SmallParams p) {
+__device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
   const int s = p.s, kp = p.kp, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nz = p.has_next ? s : 0;  // Z columns present
   __shared__ double red[kStepThreads / 32][36];
@@ -559,9 +560,44 @@ __global__ void __launch_bounds__(kStepThreads, 1) onesync_step4_kernel(SmallPar
   }
 }
 
+__global__ void __launch_bounds__(kStepThreads, 1) onesync_step4_kernel(SmallParams p) {
+  onesync_step4_body(p);
+}
+
+// gram_reduce + the one-sync step in one launch: every CTA reduces its slice of the Gram,
+// publishes it (fence + ticket), and the last CTA to finish runs the step on the complete
+// Gram (the threadfence-reduction pattern); it also re-arms the ticket for the next launch.
+static_assert(RED_THREADS == kStepThreads, "one block shape for both halves");
+__global__ void __launch_bounds__(kStepThreads, 1)
+    reduce_step4_kernel(const ReduceArgs r, SmallParams p, unsigned* ticket) {
+  __shared__ int last;
+  gram_reduce_body(r);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *ticket = 0u;
+  onesync_step4_body(p);
+}
+
+bool small_mergeable(const SmallParams& p) {
+  return p.mode == SM_ONESYNC_STEP && p.s <= 4 && p.kp <= 2 * kStepThreads && !p.sdiag_prev_copy;
+}
+
+cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallParams& p,
+                                unsigned* ticket, cudaStream_t st, int* launches) {
+  if (!small_mergeable(p)) return cudaErrorInvalidValue;
+  reduce_step4_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, kStepThreads, 0, st>>>(r, p,
+                                                                                        ticket);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches) {
   if (p.s < 1 || p.s > SMAX) return cudaErrorInvalidValue;
-  if (p.mode == SM_ONESYNC_STEP && p.s <= 4 && p.kp <= 2 * kStepThreads && !p.sdiag_prev_copy) {
+  if (small_mergeable(p)) {
     onesync_step4_kernel<<<1, kStepThreads, 0, st>>>(p);
     if (launches) *launches += 1;
     return cudaGetLastError();
