@@ -183,6 +183,11 @@ cudaError_t tsqr_tree_up_shard(double* ws, int L, int leaf_base, int Lt, int s, 
 cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s,
                                  const double* mtop, const DevStatus* status, cudaStream_t st,
                                  int* launches);
+// Apply M_leaf to one shard's Q rows, M_leaf walked down the tree from mtop in the kernel
+// (replaces tsqr_tree_down_shard + tsqr_apply_launch for s in {1, 2, 4, 8, 16}).
+cudaError_t tsqr_apply_path_shard(double* dst, long ldd, const long* d_bounds, double* ws, int L,
+                                  int leaf_base, int Lt, int s, const double* mtop,
+                                  const DevStatus* status, cudaStream_t st, int* launches);
 // Bottom-up combine of every tree t (leaves [tree_off[t], tree_off[t+1])) -> roots + t*s*s.
 cudaError_t tsqr_up_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
                            double* roots, const DevStatus* status, cudaStream_t st,

@@ -903,16 +903,14 @@ class Runner {
       Prof pr(c, "tsqr_tree", 0.0, 0.0);
       CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout,
                                 c->cross_m.d(), status, c->stream, &c->launches));
-      const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
-      for (size_t t = 0; t < sh.size(); ++t)
-        CUDA_OK(tsqr_tree_down_shard(ws, tsqr_L, sh[t].leaf_base, sh[t].n_leaves, (int)s,
-                                     mtop + t * ss, status, c->stream, &c->launches));
     }
-    for (auto& x : sh) {
+    const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
+    for (size_t t = 0; t < sh.size(); ++t) {
+      const Shard& x = sh[t];
       Prof pr(c, "tsqr_apply", 16.0 * x.rows * s, 2.0 * x.rows * s * s);
-      CUDA_OK(tsqr_apply_launch(qcol(x, dcol), x.ldq, bounds + x.bound_base, x.n_leaves, (int)s,
-                                tsqr_ws_M(ws, tsqr_L, (int)s) + (size_t)x.leaf_base * ss, status,
-                                c->stream, &c->launches));
+      CUDA_OK(tsqr_apply_path_shard(qcol(x, dcol), x.ldq, bounds + x.bound_base, ws, tsqr_L,
+                                    x.leaf_base, x.n_leaves, (int)s, mtop + t * ss, status,
+                                    c->stream, &c->launches));
     }
     record(label, (long)ss + fused_words);
   }

@@ -756,6 +756,120 @@ cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s
 }
 
 // ---------------------------------------------------------------------------------
+// Apply with the leaf's M computed on the fly (no top-down pass).  Leaf l's item index at
+// level k is l >> k; it is a pass-through where it is the odd last item, else it is half
+// (l >> k) & 1 of node nb[k] + (l >> (k + 1)).  M_leaf = H_0 H_1 ... H_{top-1} M_top with
+// H_k that half of the node's 2s x s Q — the same products, in the same order, as
+// tree_down's warp_mm, so the leaf M's are bit-identical to the top-down pass.
+// ---------------------------------------------------------------------------------
+struct TreePath {
+  int nlev;
+  int cnt[32];
+  int nb[32];
+};
+
+template <int S>
+__global__ void __launch_bounds__(256)
+    tsqr_apply_path_kernel(double* __restrict__ dst, long ldd, const long* __restrict__ leaf_row0,
+                           const double* __restrict__ nq, const double* __restrict__ mtop,
+                           const TreePath tp, const DevStatus* status) {
+  if (status && status_bad(status)) return;
+  constexpr int SS = S * S;
+  __shared__ double hq[S <= 8 ? 32 : 20][SS];  // (static shared memory <= 48 KB)
+  __shared__ double mm[2][SS];
+  const int l = blockIdx.x, tid = threadIdx.x;
+  const int nh = tp.nlev - 1;  // levels with nodes below the root
+  // every path factor at once (independent L2 reads); pass-throughs become identities
+  for (int idx = tid; idx < nh * SS; idx += blockDim.x) {
+    const int k = idx / SS, e = idx % SS, r = e % S, c = e / S;
+    const int ik = l >> k;
+    const bool pass = ik == tp.cnt[k] - 1 && (tp.cnt[k] & 1);
+    double v;
+    if (pass) {
+      v = r == c ? 1.0 : 0.0;
+    } else {
+      const int node = tp.nb[k] + (ik >> 1), half = ik & 1;
+      v = nq[(size_t)node * 2 * SS + (half * S + r) + (size_t)c * 2 * S];
+    }
+    hq[k][e] = v;
+  }
+  for (int e = tid; e < SS; e += blockDim.x)
+    mm[0][e] = mtop ? mtop[e] : ((e % S) == (e / S) ? 1.0 : 0.0);
+  __syncthreads();
+  int cur = 0;
+  if (tid < 32) {
+    for (int k = nh - 1; k >= 0; --k) {
+      const int ik = l >> k;
+      if (ik == tp.cnt[k] - 1 && (tp.cnt[k] & 1)) continue;  // pass-through: M unchanged
+      for (int e = tid; e < SS; e += 32) {
+        const int i = e % S, j = e / S;
+        double acc = 0.0;
+        for (int q = 0; q < S; ++q) acc = fma(hq[k][i + q * S], mm[cur][q + j * S], acc);
+        mm[cur ^ 1][e] = acc;
+      }
+      __syncwarp();
+      cur ^= 1;
+    }
+  }
+  __syncthreads();
+  cur = __shfl_sync(0xffffffffu, cur, 0);  // (warp 0's value; every warp reads the same)
+  __shared__ int cur_s;
+  if (tid == 0) cur_s = cur;
+  __syncthreads();
+  const double* m = mm[cur_s];
+  double mr[SS];
+#pragma unroll
+  for (int e = 0; e < SS; ++e) mr[e] = m[e];
+  const long g0 = leaf_row0[l], g1 = leaf_row0[l + 1];
+  for (long i = g0 + tid; i < g1; i += blockDim.x) {
+    double row[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) row[j] = dst[i + (size_t)j * ldd];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < S; ++k) acc = fma(row[k], mr[k + j * S], acc);
+      dst[i + (size_t)j * ldd] = acc;
+    }
+  }
+}
+
+// Q rows of one shard's leaves <- Q rows * M_leaf, with M_leaf walked down from mtop
+// (identity if null); falls back to the top-down pass + apply for other s.
+cudaError_t tsqr_apply_path_shard(double* dst, long ldd, const long* d_bounds, double* ws, int L,
+                                  int leaf_base, int Lt, int s, const double* mtop,
+                                  const DevStatus* status, cudaStream_t st, int* launches) {
+  const size_t ss = (size_t)s * s;
+  if (Lt <= 0) return cudaSuccess;
+  const TreePlan t = tree_plan(Lt, s);
+  if (t.nlev > (s <= 8 ? 32 : 20) || !(s == 1 || s == 2 || s == 4 || s == 8 || s == 16)) {
+    cudaError_t e = tsqr_tree_down_shard(ws, L, leaf_base, Lt, s, mtop, status, st, launches);
+    if (e != cudaSuccess) return e;
+    return tsqr_apply_launch(dst, ldd, d_bounds, Lt, s, ws + (size_t)2 * L * ss + (size_t)leaf_base * ss,
+                             status, st, launches);
+  }
+  TreePath tp;
+  memset(&tp, 0, sizeof tp);
+  tp.nlev = t.nlev;
+  for (int k = 0; k < t.nlev; ++k) {
+    tp.cnt[k] = t.cnt[k];
+    tp.nb[k] = t.nb[k];
+  }
+  const double* nq = ws + (size_t)4 * L * ss + (size_t)leaf_base * 2 * ss;
+#define BGS_APPLY_PATH(S_)                                                                   \
+  if (s == S_) tsqr_apply_path_kernel<S_><<<Lt, 256, 0, st>>>(dst, ldd, d_bounds, nq, mtop, tp, status);
+  BGS_APPLY_PATH(1)
+  BGS_APPLY_PATH(2)
+  BGS_APPLY_PATH(4)
+  BGS_APPLY_PATH(8)
+  BGS_APPLY_PATH(16)
+#undef BGS_APPLY_PATH
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------------
 size_t tsqr_ws_bytes(int leaves, int s) {
