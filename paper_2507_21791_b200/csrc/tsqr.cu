@@ -445,6 +445,92 @@ __device__ void warp_pair_qr(const double* top, const double* bot, int s, double
   }
 }
 
+// The same pair QR with s a template parameter: rows and reflectors in registers, and
+// reductions over the 2s active lanes only (log2 steps; the skipped xor steps would add
+// exact zeros from the idle lanes, so the results are bit-identical to warp_pair_qr).
+template <int S>
+BGS_DEV double lane_sum(double v) {
+  constexpr int W = 2 * S >= 32 ? 32 : (2 * S >= 16 ? 16 : (2 * S >= 8 ? 8 : (2 * S >= 4 ? 4 : 2)));
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return __shfl_sync(0xffffffffu, v, 0);  // warp-uniform (lanes >= W reduced only zeros)
+}
+template <int S>
+BGS_DEV double lane_max(double v) {
+  constexpr int W = 2 * S >= 32 ? 32 : (2 * S >= 16 ? 16 : (2 * S >= 8 ? 8 : (2 * S >= 4 ? 4 : 2)));
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return __shfl_sync(0xffffffffu, v, 0);  // warp-uniform: every lane takes the same branches
+}
+
+template <int S>
+__device__ void warp_pair_qr_t(const double* top, const double* bot, double* qout, double* rout) {
+  const int lane = threadIdx.x & 31;
+  constexpr int m = 2 * S;
+  double a[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j)
+    a[j] = lane < S ? top[lane + j * S] : (lane < m ? bot[(lane - S) + j * S] : 0.0);
+  double vs[S], taus[S], rd[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const double mine = (lane >= k && lane < m) ? a[k] : 0.0;
+    const double mx = lane_max<S>(fabs(mine));
+    const double akk = __shfl_sync(0xffffffffu, a[k], k);
+    if (mx == 0.0) {
+      taus[k] = 0.0; vs[k] = 0.0;
+      rd[k] = akk;
+      continue;
+    }
+    const double t = mine / mx;
+    const double ssq = lane_sum<S>(t * t);
+    const double below = lane_sum<S>(lane > k ? mine * mine : 0.0);
+    const double sigma = mx * sqrt(ssq);
+    const double alpha = akk >= 0.0 ? -sigma : sigma;
+    const double v0 = akk - alpha;
+    const double vtv = v0 * v0 + below;
+    const double tau = vtv == 0.0 ? 0.0 : 2.0 / vtv;
+    const double vi = lane == k ? v0 : (lane > k && lane < m ? a[k] : 0.0);
+#pragma unroll
+    for (int j = k + 1; j < S; ++j) {
+      const double wj = tau * lane_sum<S>(vi * a[j]);
+      a[j] -= wj * vi;
+    }
+    vs[k] = vi;
+    taus[k] = tau;
+    rd[k] = alpha;
+  }
+  double q[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) q[j] = (lane == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = S - 1; k >= 0; --k) {
+    if (taus[k] == 0.0) continue;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const double wj = taus[k] * lane_sum<S>(vs[k] * q[j]);
+      q[j] -= wj * vs[k];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const double d = rd[j];
+    const double sg = d < 0.0 ? -1.0 : 1.0;
+    if (lane < m) qout[lane + j * m] = sg * q[j];
+    if (lane == j) {
+#pragma unroll
+      for (int jj = 0; jj < S; ++jj) {
+        double v = 0.0;
+        if (jj == j) v = d;
+        else if (jj > j) v = a[jj];
+        rout[j + jj * S] = sg * v;
+      }
+    } else if (lane > j && lane < S) {
+      rout[lane + j * S] = 0.0;
+    }
+  }
+}
+
 // C = A(s x s, lda) * B(s x s); one warp.
 __device__ void warp_mm(const double* A, int lda, const double* B, int s, double* C) {
   const int lane = threadIdx.x & 31;
@@ -596,6 +682,7 @@ struct TreeGroupArgs {
   int identity_top;   // down: the top item is the identity (no M from above)
 };
 
+template <int S>  // S = 0: runtime s (generic pair QR)
 __global__ void __launch_bounds__(512) tsqr_up_group_kernel(const TreeGroupArgs a,
                                                             const DevStatus* status) {
   if (status && status_bad(status)) return;
@@ -612,9 +699,15 @@ __global__ void __launch_bounds__(512) tsqr_up_group_kernel(const TreeGroupArgs 
     const int lod = g << (D - d);
     const int nd = min(1 << (D - d), a.cnt[d] - lod);
     const int np = nd / 2;
-    for (int i = warp; i < np; i += nw)
-      warp_pair_qr(b0 + (size_t)2 * i * ss, b0 + (size_t)(2 * i + 1) * ss, s,
-                   a.nq + (size_t)(a.nb[d] + (lod >> 1) + i) * 2 * ss, b1 + (size_t)i * ss);
+    for (int i = warp; i < np; i += nw) {
+      double* qo = a.nq + (size_t)(a.nb[d] + (lod >> 1) + i) * 2 * ss;
+      if (S > 0)
+        warp_pair_qr_t<S ? S : 1>(b0 + (size_t)2 * i * ss, b0 + (size_t)(2 * i + 1) * ss, qo,
+                                  b1 + (size_t)i * ss);
+      else
+        warp_pair_qr(b0 + (size_t)2 * i * ss, b0 + (size_t)(2 * i + 1) * ss, s, qo,
+                     b1 + (size_t)i * ss);
+    }
     if (nd & 1)
       for (int e = threadIdx.x; e < ss; e += blockDim.x) b1[(size_t)np * ss + e] = b0[(size_t)(nd - 1) * ss + e];
     __syncthreads();
@@ -709,9 +802,23 @@ cudaError_t tsqr_tree_up_shard(double* ws, int L, int leaf_base, int Lt, int s, 
     a.out = j + 1 == t.launches.size() ? root_out : bufs[(j + 1) & 1];
     const int groups = (t.cnt[l0] + (1 << D) - 1) >> D;
     const size_t smem = (size_t)2 * (1 << D) * ss * sizeof(double);
-    cudaError_t e = ensure_smem(tsqr_up_group_kernel, smem);
-    if (e != cudaSuccess) return e;
-    tsqr_up_group_kernel<<<groups, 32 * std::max(1, (1 << D) / 2), smem, st>>>(a, status);
+    const int threads = 32 * std::max(1, (1 << D) / 2);
+    cudaError_t e = cudaSuccess;
+#define BGS_UP_GROUP(S_)                                                        \
+  {                                                                           \
+    e = ensure_smem(tsqr_up_group_kernel<S_>, smem);                          \
+    if (e != cudaSuccess) return e;                                           \
+    tsqr_up_group_kernel<S_><<<groups, threads, smem, st>>>(a, status);       \
+  }
+    switch (s) {
+      case 1: BGS_UP_GROUP(1) break;
+      case 2: BGS_UP_GROUP(2) break;
+      case 4: BGS_UP_GROUP(4) break;
+      case 8: BGS_UP_GROUP(8) break;
+      case 16: BGS_UP_GROUP(16) break;
+      default: BGS_UP_GROUP(0) break;
+    }
+#undef BGS_UP_GROUP
     if (launches) *launches += 1;
   }
   return cudaGetLastError();
