@@ -382,6 +382,7 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
   const int nz = p.has_next ? s : 0;  // Z columns present
   __shared__ double red[kStepThreads / 32][36];
   __shared__ double prod[36];
+  __shared__ double blk[3][16];  // Omega = G[kp:, 0:s], P = G[kp:, s:2s], T = G[kp+s:, s:2s]
   __shared__ int bad_flag;
   if (tid == 0) bad_flag = 0;
   // previous S_diag (broadcast loads) and the status word, issued together
@@ -389,6 +390,16 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) sdp[e] = ((e & 3) < s && (e >> 2) < s) ? p.sdiag[(e & 3) + s * (e >> 2)] : 0.0;
   const bool dead = status_bad(p.status);
+  if (tid < 48) {  // the s x s blocks thread 0 needs later, loaded now in parallel
+    const int b = tid >> 4, e = tid & 15, i = e & 3, j = e >> 2;
+    double v = 0.0;
+    if (i < s && j < s && (b == 0 || p.has_next)) {
+      const size_t ld = p.ldg;
+      v = b == 0 ? p.G[(kp + i) + j * ld]
+                 : b == 1 ? p.G[(kp + i) + (s + j) * ld] : p.G[(kp + s + i) + (s + j) * ld];
+    }
+    blk[b][e] = v;
+  }
   // ---- one pass over rows: products, R column, scol_next copy, non-finite check ----
   double acc[36];
 #pragma unroll
@@ -467,9 +478,7 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
   }
   __syncthreads();
   if (tid != 0) return;
-  // ---- thread 0: s x s factors in registers ----
-  const double* G = p.G;
-  const size_t ld = p.ldg;
+  // ---- thread 0: s x s factors in registers (the s x s Gram blocks come from blk) ----
   double ytz[16], c[16], yd[16], sd[16];
   {
     int e = 0;
@@ -490,7 +499,7 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        c[i + 4 * j] = (i < s && j < s) ? G[(kp + i) + j * ld] - yty[i + 4 * j] : 0.0;
+        c[i + 4 * j] = (i < s && j < s) ? blk[0][i + 4 * j] - yty[i + 4 * j] : 0.0;
   }
   int piv = chol4(c, s, yd);
   if (piv) {
@@ -521,7 +530,7 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      bm[i + 4 * j] = (i < s && j < s) ? G[(kp + i) + (s + j) * ld] - ytz[i + 4 * j] : 0.0;
+      bm[i + 4 * j] = (i < s && j < s) ? blk[1][i + 4 * j] - ytz[i + 4 * j] : 0.0;
   piv = trsm4(yd, bm, s, s2);
   if (piv) {
     set_status(p.status, ST_SINGULAR, piv, p.k + 1, SITE_NONE, 0);
@@ -543,8 +552,8 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
         double a = prod[e++];
 #pragma unroll
         for (int k = 0; k < 4; ++k) a += s2[k + 4 * i] * s2[k + 4 * j];
-        const double v = (i < s && j < s) ? G[(kp + s + i) + (s + j) * ld] : 0.0;
-        const double vt = (i < s && j < s) ? G[(kp + s + j) + (s + i) * ld] : 0.0;
+        const double v = (i < s && j < s) ? blk[2][i + 4 * j] : 0.0;
+        const double vt = (i < s && j < s) ? blk[2][j + 4 * i] : 0.0;
         t[i + 4 * j] = v - a;
         t[j + 4 * i] = vt - a;
       }
