@@ -511,9 +511,10 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
 // Host side
 // ------------------------------------------------------------------------------------
 namespace {
-// instances: KW k-steps per warp in {2, 4, ..., 16} for each R; MTW covers the output
-// tiles the plan can give a warp at that KW (C = 1: mt <= KS KW / 2 + 3)
-__host__ __device__ constexpr int mtw_for(int kw, int R) { return ((4 / R) * kw / 2 + 3 + 3) / 4; }
+// instances: KW k-steps per warp in 1..16 for each R; MTW covers the output tiles a warp
+// can get at that KW: a rank's prefix of KS KW k-steps spans <= KS KW / 2 units, plus the
+// A-block unit and one span-1 unit -> mt <= KS KW / 2 + 2 (C = 1 and C = 2 alike)
+__host__ __device__ constexpr int mtw_for(int kw, int R) { return ((4 / R) * kw / 2 + 2 + 3) / 4; }
 constexpr int kKwMax = 16;
 
 struct Cand {
@@ -563,8 +564,8 @@ bool k12_plan(SplitParams& p) {
     const int kw = (std::max(k0, k1) + KS - 1) / KS;
     const int mtw = (std::max(mt0, mt1) + kGroupWarps - 1) / kGroupWarps;
     const int kw_max = kKwMax;
-    int kw_t = std::max(2, (kw + 1) / 2 * 2);
-    while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) kw_t += 2;
+    int kw_t = std::max(1, kw);
+    while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) ++kw_t;
     if (kw_t > kw_max) continue;
     const char* me = getenv("BGS_K12C_MINS");  // experiments: minimum ring depth (default 3)
     const int min_s = me ? std::max(2, atoi(me)) : 3;
@@ -609,14 +610,11 @@ static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
 template <int R>
 static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
   switch (p.kw) {
-    case 2: return launch_k12<2, R>(p, grid, st);
-    case 4: return launch_k12<4, R>(p, grid, st);
-    case 6: return launch_k12<6, R>(p, grid, st);
-    case 8: return launch_k12<8, R>(p, grid, st);
-    case 10: return launch_k12<10, R>(p, grid, st);
-    case 12: return launch_k12<12, R>(p, grid, st);
-    case 14: return launch_k12<14, R>(p, grid, st);
-    case 16: return launch_k12<16, R>(p, grid, st);
+#define BGS_KW(K) \
+  case K: return launch_k12<K, R>(p, grid, st);
+    BGS_KW(1) BGS_KW(2) BGS_KW(3) BGS_KW(4) BGS_KW(5) BGS_KW(6) BGS_KW(7) BGS_KW(8)
+    BGS_KW(9) BGS_KW(10) BGS_KW(11) BGS_KW(12) BGS_KW(13) BGS_KW(14) BGS_KW(15) BGS_KW(16)
+#undef BGS_KW
     default: return cudaErrorInvalidValue;
   }
 }

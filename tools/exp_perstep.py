@@ -21,6 +21,6 @@ tot = 0.0
 for k, d in rows:
     tot += d["ms"]
     kp = int(k.split("kp")[1])
-    if kp % 20 == 0 or kp <= 12 or kp >= 388:
+    if os.environ.get("ALLSTEPS") or kp % 20 == 0 or kp <= 12 or kp >= 388:
         print(f"kp {kp:4d}  ms {d['ms']/d['launches']:.4f}  GB/s {d['alg_bytes']/d['ms']/1e6:7.1f}")
 print("fused total ms", round(tot, 3), "launches", sum(d["launches"] for _, d in rows))
