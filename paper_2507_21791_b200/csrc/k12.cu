@@ -36,6 +36,7 @@
 // units.  The two groups' double-doubles are combined in the CTA at the end; one partial
 // slot per cluster (every tile written by exactly one rank) -> gram_reduce.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -580,6 +581,10 @@ bool k12_plan(SplitParams& p) {
     q.mtw = mtw_for(kw_t, cd.R);
     q.stages = S;
     p = q;
+    static const bool verbose = getenv("BGS_K12C_VERBOSE") != nullptr;
+    if (verbose)
+      fprintf(stderr, "[k12c plan] kp %d U0 %d: C %d R %d KW %d (need %d) MTW %d (need %d) S %d slot %d units\n",
+              p.kp, p.U0, p.cluster, p.R, p.kw, kw, p.mtw, mtw, p.stages, p.slot_units);
     return true;
   }
   return false;
