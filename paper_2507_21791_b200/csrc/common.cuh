@@ -243,11 +243,4 @@ BGS_DEV void bar_named(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-// Swizzled (CU_TENSOR_MAP_SWIZZLE_128B) byte offset of the 16-byte chunk `chunk`
-// (rows 2*chunk, 2*chunk+1) of tile column `col` inside a box of 8 columns x 16 rows.
-// Each box is one 1024-byte swizzle atom.
-BGS_DEV uint32_t swz(int col, int chunk) {
-  return static_cast<uint32_t>((col >> 3) * 1024 + (col & 7) * 128 + ((chunk ^ (col & 7)) << 4));
-}
-
 }  // namespace bgs

@@ -188,15 +188,7 @@ cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s
 cudaError_t tsqr_apply_path_shard(double* dst, long ldd, const long* d_bounds, double* ws, int L,
                                   int leaf_base, int Lt, int s, const double* mtop,
                                   const DevStatus* status, cudaStream_t st, int* launches);
-// Bottom-up combine of every tree t (leaves [tree_off[t], tree_off[t+1])) -> roots + t*s*s.
-cudaError_t tsqr_up_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
-                           double* roots, const DevStatus* status, cudaStream_t st,
-                           int* launches);
-// Top-down: per-leaf M (region M) from each tree's root matrix mtop + t*s*s.
-cudaError_t tsqr_down_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
-                             const double* mtop, const DevStatus* status, cudaStream_t st,
-                             int* launches);
-// Q rows of leaf l <- Q rows * M_l (in place).
+// Q rows of leaf l <- Q rows * M_l (in place; M_l precomputed by tsqr_tree_down_shard).
 cudaError_t tsqr_apply_launch(double* dst, long ldd, const long* d_bounds, int L, int s,
                               const double* M, const DevStatus* status, cudaStream_t st,
                               int* launches);
@@ -217,8 +209,5 @@ cudaError_t residual_launch(const double* x, long ldx, const double* q, long ldq
                             const double* r, long ldr, long n_rows, long m, double inv_scale_d,
                             double inv_scale_x, double* ws, double* out, int num_sms,
                             cudaStream_t st);
-cudaError_t maxabs_launch(const double* x, long ldx, long n_rows, long m, double* ws,
-                          double* out, int num_sms, cudaStream_t st);
-cudaError_t sum_into_launch(double* dst, const double* src, long count, cudaStream_t st);
 
 }  // namespace bgs

@@ -189,21 +189,4 @@ cudaError_t ensure_smem_impl(const void* kernel, size_t bytes) {
   return e;
 }
 
-cudaError_t maxabs_launch(const double*, long, long, long, double*, double*, int, cudaStream_t) {
-  return cudaSuccess;
-}
-
-__global__ void sum_into_kernel(double* dst, const double* src, long count) {
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count;
-       i += (long)gridDim.x * blockDim.x)
-    dst[i] += src[i];
-}
-
-cudaError_t sum_into_launch(double* dst, const double* src, long count, cudaStream_t st) {
-  if (count <= 0) return cudaSuccess;
-  sum_into_kernel<<<(int)((count + 255) / 256 < 1024 ? (count + 255) / 256 : 1024), 256, 0, st>>>(
-      dst, src, count);
-  return cudaGetLastError();
-}
-
 }  // namespace bgs

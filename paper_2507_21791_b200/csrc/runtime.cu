@@ -206,7 +206,7 @@ struct bgs_ctx {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> xfer_events;  // reusable, timing disabled
   DBuf partial, G, scolA, scolB, sdiag, ydiag, save, r1, r2, rtop, R, status;
-  DBuf tsqr_ws, tsqr_bounds, tsqr_trees, roots, roots_all, cross_ws, cross_m, metrics;
+  DBuf tsqr_ws, tsqr_bounds, roots, roots_all, cross_ws, cross_m, metrics;
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
   std::vector<DBuf> rscr;    // per-shard right-operand scratch of chunked Grams
   DBuf ticket;               // last-CTA ticket of the merged reduce + step kernel
@@ -253,7 +253,7 @@ struct bgs_ctx {
   }
   ~bgs_ctx() {
     for (DBuf* b : {&partial, &G, &scolA, &scolB, &sdiag, &ydiag, &save, &r1, &r2, &rtop, &R,
-                    &status, &tsqr_ws, &tsqr_bounds, &tsqr_trees, &roots, &roots_all, &cross_ws,
+                    &status, &tsqr_ws, &tsqr_bounds, &roots, &roots_all, &cross_ws,
                     &cross_m, &metrics})
       b->release();
     for (auto& b : sx) b.release();
@@ -445,7 +445,6 @@ class Runner {
     // TSQR leaf plan
     const long lw = s <= 4 ? 1024 : (s <= 8 ? 512 : 256);
     std::vector<long> bounds;
-    std::vector<int> trees;
     int leaf = 0;
     for (auto& x : sh) {
       long L = x.rows <= 0 ? 1 : (x.rows + lw - 1) / lw;
@@ -459,17 +458,12 @@ class Runner {
         bounds.push_back(b);
         if (l > 0) x.hmax = std::max(x.hmax, b - bounds[bounds.size() - 2]);
       }
-      trees.push_back(leaf);
       leaf += (int)L;
     }
-    trees.push_back(leaf);
     tsqr_L = leaf;
     c->tsqr_ws.ensure(tsqr_ws_bytes(tsqr_L, (int)s) + 64);
     c->tsqr_bounds.ensure(bounds.size() * sizeof(long));
-    c->tsqr_trees.ensure(trees.size() * sizeof(int));
     CUDA_OK(cudaMemcpyAsync(c->tsqr_bounds.p, bounds.data(), bounds.size() * sizeof(long),
-                            cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaMemcpyAsync(c->tsqr_trees.p, trees.data(), trees.size() * sizeof(int),
                             cudaMemcpyHostToDevice, c->stream));
     c->roots.ensure((size_t)sh.size() * ss * sizeof(double) + 64);
     c->roots_all.ensure((size_t)P * ss * sizeof(double) + 64);

@@ -616,22 +616,6 @@ __device__ void tree_down(TreeWs w, int off, int c, int s, const double* mtop) {
   }
 }
 
-__global__ void tsqr_up_kernel(const int* tree_off, double* ws, int L, int s, double* roots,
-                               const DevStatus* status) {
-  if (status && status_bad(status)) return;
-  const int t = blockIdx.x;
-  const int off = tree_off[t], c = tree_off[t + 1] - tree_off[t];
-  tree_up(tree_ws(ws, L, s), off, c, s, roots + (size_t)t * s * s, s);
-}
-
-__global__ void tsqr_down_kernel(const int* tree_off, double* ws, int L, int s,
-                                 const double* mtop, const DevStatus* status) {
-  if (status && status_bad(status)) return;
-  const int t = blockIdx.x;
-  const int off = tree_off[t], c = tree_off[t + 1] - tree_off[t];
-  tree_down(tree_ws(ws, L, s), off, c, s, mtop ? mtop + (size_t)t * s * s : nullptr);
-}
-
 __global__ void tsqr_cross_kernel(const double* roots, int n, int s, double* ws2, double* rout,
                                   int ldr, double* mout, const DevStatus* status) {
   if (status && status_bad(status)) return;
@@ -1007,22 +991,6 @@ cudaError_t tsqr_leaf_launch(const double* src, long lds, double* dst, long ldd,
   cudaError_t e = ensure_smem(tsqr_leaf_kernel, smem);
   if (e != cudaSuccess) return e;
   tsqr_leaf_kernel<<<L, kLeafThreads, smem, st>>>(src, lds, dst, ldd, d_bounds, s, rleaf, status);
-  if (launches) *launches += 1;
-  return cudaGetLastError();
-}
-
-cudaError_t tsqr_up_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
-                           double* roots, const DevStatus* status, cudaStream_t st,
-                           int* launches) {
-  tsqr_up_kernel<<<n_trees, 512, 0, st>>>(d_tree_off, ws, L, s, roots, status);
-  if (launches) *launches += 1;
-  return cudaGetLastError();
-}
-
-cudaError_t tsqr_down_launch(int n_trees, const int* d_tree_off, double* ws, int L, int s,
-                             const double* mtop, const DevStatus* status, cudaStream_t st,
-                             int* launches) {
-  tsqr_down_kernel<<<n_trees, 512, 0, st>>>(d_tree_off, ws, L, s, mtop, status);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
