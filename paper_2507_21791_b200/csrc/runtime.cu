@@ -893,18 +893,22 @@ class Runner {
       NCCL_OK(nccl().GroupEnd());
       all_roots = c->roots_all.d();
     }
-    {
+    const double* mtop = nullptr;  // identity: a single shard's root is the global root
+    if (P == 1 && sh.size() == 1) {
+      CUDA_OK(cudaMemcpy2DAsync(rout, (size_t)ldrout * sizeof(double), all_roots, s * sizeof(double),
+                                s * sizeof(double), s, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
       Prof pr(c, "tsqr_tree", 0.0, 0.0);
       CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout,
                                 c->cross_m.d(), status, c->stream, &c->launches));
+      mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
     }
-    const double* mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
     for (size_t t = 0; t < sh.size(); ++t) {
       const Shard& x = sh[t];
       Prof pr(c, "tsqr_apply", 16.0 * x.rows * s, 2.0 * x.rows * s * s);
       CUDA_OK(tsqr_apply_path_shard(qcol(x, dcol), x.ldq, bounds + x.bound_base, ws, tsqr_L,
-                                    x.leaf_base, x.n_leaves, (int)s, mtop + t * ss, status,
-                                    c->stream, &c->launches));
+                                    x.leaf_base, x.n_leaves, (int)s, mtop ? mtop + t * ss : nullptr,
+                                    status, c->stream, &c->launches));
     }
     record(label, (long)ss + fused_words);
   }
