@@ -220,7 +220,7 @@ __device__ __forceinline__ void cta_sum_t(double (&v)[NV], double* scratch /*[8]
 }
 
 template <int S, int RPT>
-__global__ void __launch_bounds__(kLeafThreads)
+__global__ void __launch_bounds__(kLeafThreads, S <= 4 ? 3 : 1)  // 3 leaves per SM for s <= 4
     tsqr_leaf_reg_kernel(const double* __restrict__ src, long lds, double* __restrict__ dst,
                          long ldd, const long* __restrict__ leaf_row0,
                          double* __restrict__ rleaf, const DevStatus* status) {
