@@ -93,6 +93,11 @@ int bgs_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
                    bgs_ctx** out, bgs_error* err);
 void bgs_ctx_destroy(bgs_ctx* ctx);
 int bgs_nccl_unique_id(void* out128, bgs_error* err); /* ncclGetUniqueId via the ctx's NCCL */
+/* The *_device entry points below run on the context's own stream and first wait (an
+ * event, no host sync) for all work queued so far on the caller's stream, so buffers the
+ * caller filled asynchronously are safe to pass.  Default: the legacy default stream
+ * (torch's default).  `stream` is a cudaStream_t.  Results are complete on return. */
+int bgs_ctx_set_stream(bgs_ctx* ctx, void* stream);
 int bgs_device_info(int device, int* sm_count, long* hbm_bytes, char* name, long name_cap);
 
 /* ---- drop-in for run_factor (runner.hpp:28-29, runner.cpp:39-67) ------------------

@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import os
+import sys
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional
 
@@ -144,6 +145,7 @@ def _load() -> ctypes.CDLL:
         "bgs_shard_rows": ([L, I, I, P, P], I),
         "bgs_ctx_create": ([I, I, I, P, P, P], I),
         "bgs_ctx_destroy": ([P], None),
+        "bgs_ctx_set_stream": ([P, P], I),
         "bgs_nccl_unique_id": ([P, P], I),
         "bgs_device_info": ([I, P, P, P, L], I),
         "bgs_factor": ([P, I, L, L, L, I, P, L, P, L, P, L, P, P, P], I),
@@ -168,7 +170,8 @@ _lib = _load()
 
 EXPORTED_SYMBOLS = (
     "bgs_variant_name", "bgs_parse_variant", "bgs_expected_syncs", "bgs_variant_flops",
-    "bgs_shard_rows", "bgs_ctx_create", "bgs_ctx_destroy", "bgs_nccl_unique_id",
+    "bgs_shard_rows", "bgs_ctx_create", "bgs_ctx_destroy", "bgs_ctx_set_stream",
+    "bgs_nccl_unique_id",
     "bgs_device_info", "bgs_factor", "bgs_factor_device", "bgs_gen_gaussian_device",
     "bgs_gen_gaussian_host", "bgs_metrics", "bgs_metrics_device", "bgs_gram", "bgs_tsqr",
     "bgs_profile_enable", "bgs_profile_read",
@@ -306,6 +309,17 @@ class Context:
     @property
     def handle(self) -> ctypes.c_void_p:
         return self._h
+
+    def set_stream(self, stream: int) -> None:
+        """cudaStream_t (as an int) whose queued work the *_device calls wait for."""
+        _lib.bgs_ctx_set_stream(self._h, ctypes.c_void_p(int(stream) or None))
+
+    def _follow_torch(self) -> None:
+        # Device buffers usually come from torch, whose work is queued on its current
+        # stream: make the library wait for it (an event; no host synchronisation).
+        torch = sys.modules.get("torch")
+        if torch is not None and torch.cuda.is_initialized():
+            self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     def profile(self, on: bool = True) -> None:
         """Bracket every kernel class of the factorization with CUDA events."""
@@ -464,6 +478,7 @@ def factor_device(ctx: Context, v: int, n: int, m: int, s: int, row0: int, n_loc
                   ) -> tuple[np.ndarray, SyncStats, Timing]:
     r = np.zeros((m, m), dtype=np.float64, order="F")
     st, tm, err = _Stats(), _Timing(), _Err()
+    ctx._follow_torch()
     rc = _lib.bgs_factor_device(ctx.handle, int(v), n, m, s, row0, n_local, x_ptr, ldx, q_ptr,
                                 ldq, _ptr(r), m, ctypes.byref(st), ctypes.byref(tm),
                                 ctypes.byref(err))
@@ -474,6 +489,7 @@ def factor_device(ctx: Context, v: int, n: int, m: int, s: int, row0: int, n_loc
 def gen_gaussian_device(ctx: Context, seed: int, row0: int, n_local: int, m: int, x_ptr: int,
                         ldx: int) -> None:
     err = _Err()
+    ctx._follow_torch()
     rc = _lib.bgs_gen_gaussian_device(ctx.handle, int(seed), row0, n_local, m, x_ptr, ldx,
                                       ctypes.byref(err))
     _raise(rc, err)
@@ -483,6 +499,7 @@ def metrics_device(ctx: Context, n: int, m: int, n_local: int, x_ptr: int, ldx: 
                    q_ptr: int, ldq: int, r: np.ndarray) -> tuple[float, float]:
     rf = _fortran(r)
     loo, res, err = ctypes.c_double(), ctypes.c_double(), _Err()
+    ctx._follow_torch()
     rc = _lib.bgs_metrics_device(ctx.handle, n, m, n_local, x_ptr, ldx, q_ptr, ldq, _ptr(rf), m,
                                  ctypes.byref(loo), ctypes.byref(res), ctypes.byref(err))
     _raise(rc, err)

@@ -202,6 +202,11 @@ struct bgs_ctx {
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // The device-pointer entry points run on `stream` (non-blocking) but first wait for the
+  // caller's work issued so far on `caller` (legacy default stream unless set with
+  // bgs_ctx_set_stream): a buffer the caller filled or cleared asynchronously is ready.
+  cudaStream_t caller = nullptr;
+  cudaEvent_t entry = nullptr;
   // copy engines of the host drop-in (bgs_factor): X chunks in, final Q columns out
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> xfer_events;  // reusable, timing disabled
@@ -268,6 +273,7 @@ struct bgs_ctx {
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
+    if (entry) cudaEventDestroy(entry);
     for (auto e : xfer_events) cudaEventDestroy(e);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
@@ -278,6 +284,12 @@ struct bgs_ctx {
 namespace {
 
 static long even_ld(long rows) { return std::max<long>(32, (rows + 31) & ~31L); }
+
+// Order the context stream after everything the caller has queued on its stream.
+static void order_after_caller(bgs_ctx* c) {
+  CUDA_OK(cudaEventRecord(c->entry, c->caller));
+  CUDA_OK(cudaStreamWaitEvent(c->stream, c->entry, 0));
+}
 
 // One row shard resident on this device: rows [row0, row0 + rows) of the global matrix.
 struct Shard {
@@ -1469,6 +1481,7 @@ int bgs_ctx_create(int device, int rank, int nranks, const void* uid, bgs_ctx** 
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreate(&c->e0));
     CUDA_OK(cudaEventCreate(&c->e1));
+    CUDA_OK(cudaEventCreateWithFlags(&c->entry, cudaEventDisableTiming));
     if (nranks > 1) {
       if (!uid) fail(BGS_E_COLLECTIVE, "nranks > 1 needs an ncclUniqueId");
       if (!nccl().ok) fail(BGS_E_COLLECTIVE, "libnccl.so.2 could not be loaded");
@@ -1483,6 +1496,12 @@ int bgs_ctx_create(int device, int rank, int nranks, const void* uid, bgs_ctx** 
     put_err(err, f);
     return f.code;
   }
+}
+
+int bgs_ctx_set_stream(bgs_ctx* c, void* stream) {
+  if (!c) return BGS_E_CUDA;
+  c->caller = static_cast<cudaStream_t>(stream);
+  return BGS_OK;
 }
 
 void bgs_ctx_destroy(bgs_ctx* c) {
@@ -1632,6 +1651,7 @@ int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0
            e0r + erows);
     if (ldx < n_local || ldq < n_local || ldr < m) fail(BGS_E_DIMENSION, "leading dimension too small");
     select_device(c);
+    order_after_caller(c);
     Runner run(c, variant, n, m, s, c->nranks, c->nranks > 1, stats);
     Shard sh;
     sh.row0 = row0;
@@ -1679,6 +1699,7 @@ int bgs_gen_gaussian_device(bgs_ctx* c, unsigned long long seed, long row0, long
   clear_err(err);
   try {
     select_device(c);
+    order_after_caller(c);
     CUDA_OK(gen_gaussian_launch(seed, row0, n_local, m, d_x, ldx, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
     return BGS_OK;
@@ -1722,6 +1743,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
   clear_err(err);
   try {
     select_device(c);
+    order_after_caller(c);
     (void)n;
     const int si = 8;
     // Q^T Q in panels of 8 right columns through K1 (+ NCCL allreduce)

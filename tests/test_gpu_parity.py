@@ -366,6 +366,35 @@ def test_factor_device_ignores_stale_q(gpu_ctx, s):
     assert np.abs(r - ref.r).max() <= 1e-12 * np.abs(ref.r).max()
 
 
+@pytest.mark.parametrize("side_stream", [False, True])
+def test_device_entry_waits_for_callers_stream(gpu_ctx, side_stream):
+    """The *_device calls run on the context's own stream: they must first wait for the
+    caller's queued work (here a ~20 ms spin, then the fill of X and the clearing of Q)
+    on torch's current stream, default or side stream, with no host sync in between."""
+    import torch
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 200_003, 64, 4
+    ld = (n + 31) // 32 * 32
+    x = bgs.gen_gaussian_host(4242, n, m)
+    src = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    src[:, :n] = torch.from_numpy(np.asfortranarray(x).T.copy()).cuda()
+    X = torch.zeros_like(src)
+    Q = torch.full_like(src, float("nan"))
+    torch.cuda.synchronize()
+    st_ = torch.cuda.Stream() if side_stream else torch.cuda.current_stream()
+    with torch.cuda.stream(st_):
+        torch.cuda._sleep(40_000_000)
+        X.copy_(src)
+        Q.zero_()
+        r, st, tm = bgs.factor_device(gpu_ctx, 3, n, m, s, 0, n, X.data_ptr(), ld,
+                                      Q.data_ptr(), ld)
+        loo, res = bgs.metrics_device(gpu_ctx, n, m, n, X.data_ptr(), ld, Q.data_ptr(), ld, r)
+    ref = bgs.run_factor(3, x, s, 1, metrics=False, ctx=gpu_ctx)
+    assert np.abs(r - ref.r).max() <= 1e-12 * np.abs(ref.r).max()
+    assert loo < 1e-14 and res < 1e-14, (loo, res)
+    torch.cuda.synchronize()
+
+
 def test_geometric_kappa_1e6_matches_oracle(oracle, gpu_ctx):
     """Config 5's matrix family (X = U diag(sigma) V^T, sigma log-spaced 1..1e-6) at reduced
     size on the oracle's own bits: the orthogonality loss tracks the reference's."""
@@ -391,3 +420,50 @@ def test_gpu_geometric_generator(gpu_ctx):
     matgen.geometric_device(gpu_ctx, n, m, 1e4, 7, 0, n, X, ld)
     sv = np.linalg.svd(X[:, :n].cpu().numpy().T, compute_uv=False)
     assert np.allclose(sv, matgen.sigma_schedule(m, 1e4), rtol=1e-10, atol=0)
+
+
+# ---------------------------------------------------------------------------------------
+# Full BASELINE sizes through size-independent properties (the oracle would take hours)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("v", VARIANTS, ids=lambda v: NAMES[v])
+def test_config2_full_size_properties(gpu_ctx, v):
+    """n = 1e6, m = 400, s = 4, N(0,1): exact sync accounting, exact-zero lower triangle,
+    nonnegative diagonal, and orthogonality / residual at the u level (double-double
+    metrics on the device; the reference reports ~1e-15 for this family)."""
+    import torch
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 1_000_000, 400, 4
+    ld = (n + 31) // 32 * 32
+    X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
+    Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    bgs.gen_gaussian_device(gpu_ctx, 12345, 0, n, m, X.data_ptr(), ld)
+    r, st, tm = bgs.factor_device(gpu_ctx, v, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+    assert st.sync_count == bgs.expected_syncs(v, m // s)
+    assert_structure(r)
+    loo, res = bgs.metrics_device(gpu_ctx, n, m, n, X.data_ptr(), ld, Q.data_ptr(), ld, r)
+    assert loo < 1e-14 and res < 1e-14, (loo, res)
+
+
+def test_config5_full_size_orthogonality_loss(gpu_ctx):
+    """n = 1e7, m = 400, X = U diag(sigma) V^T, kappa = 1e6 (BASELINE config 5, generated on
+    the GPU): P-1S keeps the orthogonality loss at the u level (u kappa^2 = 1e-4 <= 1)."""
+    import torch
+    import paper_2507_21791_b200 as bgs
+    from paper_2507_21791_b200 import matgen
+    n, m, s = 10_000_000, 400, 4
+    ld = (n + 31) // 32 * 32
+    X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
+    Q = torch.empty((m, ld), dtype=torch.float64, device="cuda")
+    matgen.geometric_device(gpu_ctx, n, m, 1e6, 12345, 0, n, X, ld, scratch=Q)
+    Q.zero_()
+    r, st, tm = bgs.factor_device(gpu_ctx, 3, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+    assert st.sync_count == bgs.expected_syncs(3, m // s)
+    assert_structure(r)
+    sv = np.linalg.svd(r, compute_uv=False)  # R carries X's spectrum
+    # singular values of R = those of X = sigma (to ~u kappa relative in the tail)
+    assert np.allclose(sv, matgen.sigma_schedule(m, 1e6), rtol=1e-3, atol=0)
+    assert np.allclose(sv[:200], matgen.sigma_schedule(m, 1e6)[:200], rtol=1e-9, atol=0)
+    loo, res = bgs.metrics_device(gpu_ctx, n, m, n, X.data_ptr(), ld, Q.data_ptr(), ld, r)
+    assert loo < 1e-13 and res < 1e-14, (loo, res)
+    del X, Q
+    torch.cuda.empty_cache()
