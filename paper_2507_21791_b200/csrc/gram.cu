@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant
 
 // Deterministic cross-CTA reduction in double-double, rank-local (reduce.cuh).
 __global__ void __launch_bounds__(RED_THREADS) gram_reduce_kernel(const ReduceArgs a) {
-  gram_reduce_body(a);
+  gram_reduce_body(a, blockIdx.x);
 }
 
 // ------------------------------------------------------------------------------------

@@ -163,7 +163,7 @@ bool small_mergeable(const SmallParams& p);
 cudaError_t gram_reduce_launch_args(const ReduceArgs& a, int entries, cudaStream_t st,
                                     int* launches);
 cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallParams& p,
-                                unsigned* ticket, cudaStream_t st, int* launches);
+                                unsigned* ticket, int sms, cudaStream_t st, int* launches);
 
 // ---------------- K4: TSQR (tsqr.cu) ----------------
 // Workspace for a TSQR over L leaves of width s: regions [R | Rtmp | M | Mtmp] of

@@ -22,12 +22,14 @@ struct ReduceArgs {
   double* out;
 };
 
-// Block b reduces entries [b * RED_ENTRIES, (b + 1) * RED_ENTRIES); every thread returns
-// (the block barrier inside is reached by all of them).
-BGS_DEV void gram_reduce_body(const ReduceArgs& a) {
+// Entry block b reduces entries [b * RED_ENTRIES, (b + 1) * RED_ENTRIES); every thread
+// returns (the block barrier inside is reached by all of them).  A CTA may run several
+// entry blocks in a row: the barrier at entry protects the shared slice sums of the
+// previous one.
+BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b) {
   __shared__ double2 red[RED_SLICES][RED_ENTRIES];
   const int le = threadIdx.x % RED_ENTRIES, sl = threadIdx.x / RED_ENTRIES;
-  const int idx = blockIdx.x * RED_ENTRIES + le;
+  const int idx = b * RED_ENTRIES + le;
   const int per_cta = a.mt_out * 8 * a.N8;
   double s = 0.0, e = 0.0;
   if (idx < per_cta) {
@@ -48,6 +50,7 @@ BGS_DEV void gram_reduce_body(const ReduceArgs& a) {
       }
     }
   }
+  __syncthreads();
   red[sl][le] = make_double2(s, e);
   __syncthreads();
   if (sl != 0 || idx >= per_cta) return;

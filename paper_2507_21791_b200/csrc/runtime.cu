@@ -544,7 +544,11 @@ class Runner {
       const char* e = getenv("BGS_PROF_MINKP");
       return e ? atoi(e) : 0;
     }();
-    if (tile_prof && fz.kp >= prof_minkp) {
+    static const int prof_maxkp = [] {
+      const char* e = getenv("BGS_PROF_MAXKP");
+      return e ? atoi(e) : 1 << 30;
+    }();
+    if (tile_prof && fz.kp >= prof_minkp && fz.kp <= prof_maxkp) {
       c->metrics.ensure((size_t)512 * 16 * sizeof(unsigned long long) + 64);
       p.phase = reinterpret_cast<unsigned long long*>(c->metrics.p) + 256 * 16;
     }
@@ -860,11 +864,17 @@ class Runner {
     p.R = c->R.d();
     p.ldr = (int)m;
     p.status = status;
+    static const int exp_skip = getenv("BGS_EXP_SKIP_SMALL") ? atoi(getenv("BGS_EXP_SKIP_SMALL")) : 0;
+    if (exp_skip && pend.on && small_mergeable(p)) {  // TEMP experiment: 1 = skip both, 2 = reduce only
+      pend.on = false;
+      if (exp_skip == 2) CUDA_OK(gram_reduce_launch_args(pend.a, pend.entries, c->stream, &c->launches));
+      return;
+    }
     if (pend.on && small_mergeable(p)) {
       pend.on = false;
       Prof pr(c, "reduce_small", pend.bytes, 0.0);
       CUDA_OK(reduce_small_launch(pend.a, pend.entries, p, static_cast<unsigned*>(c->ticket.p),
-                                  c->stream, &c->launches));
+                                  c->sms, c->stream, &c->launches));
       return;
     }
     flush_reduce();

@@ -11,6 +11,8 @@
 // 1-based pivot, NotSpd diagnostics {site, block column, assumption power}, and the
 // NonFiniteError check on every reduced Gram (dense_kernels.cpp:45-47).  Results go to
 // device buffers read by K2; the host never waits on them.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "reduce.cuh"
@@ -318,79 +320,126 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
 }
 
 // ---------------------------------------------------------------------------------
-// SM_ONESYNC_STEP for s <= 4 (bcgs.cpp:294-367), the per-step op of the one-sync sweep:
-// one pass over the kp rows of [Y | Z] = G[0:kp, 0:2s] computes Y^T Y, Y^T Z, Z^T Z (36
-// dot products per thread, then a fixed-order block reduction), the R column
-// S_prev + Y S_diag and the copy of Z into scol_next; thread 0 then runs the s x s
-// Cholesky / triangular solves in registers.  Same operation order as chol_serial /
-// trsm_lt_serial / r_diag; only the kp-long sums are grouped differently (the reference
-// forms them sequentially, this path by rows-per-thread then a tree).
+// SM_ONESYNC_STEP for s <= 4 (bcgs.cpp:294-367), the per-step op of the one-sync sweep.
+// It sits on the critical path between two fused kernels, so it is built for latency:
+//  1. one coalesced pass over the kp rows of [Y | Z] = G[0:kp, 0:2s]: the R column
+//     S_prev + Y S_diag, the copy of Z into scol_next, the non-finite check, and the rows
+//     staged in shared memory;
+//  2. Y^T Y, Y^T Z, Z^T Z as 36 products x 7 row chunks on 252 threads (two interleaved
+//     accumulators per thread), then a fixed-order sum of the chunks;
+//  3. the s x s factors on lanes 0..3 of warp 0, lane j owning column j: Cholesky row by
+//     row (the diagonal on lane i, then the divisions of row i in parallel), triangular
+//     solves column-parallel.
+// Every entry is formed by the same expression as chol_serial / trsm_lt_serial / r_diag
+// (symmetrization, the k-ordered updates, the !(acc > 0) pivot test, division by the
+// diagonal); only the kp-long sums are grouped differently (the reference forms them
+// sequentially, this path by row chunks).
 // ---------------------------------------------------------------------------------
 namespace {
 constexpr int kStepThreads = 256;
+constexpr int kStepRowsMax = 2 * kStepThreads;  // small_mergeable: kp <= 512
+constexpr int kStepChunks = 7;                  // 36 x 7 = 252 product threads
+constexpr int kYZLd = kStepRowsMax + 1;         // odd column stride: columns in distinct banks
 
-// upper Cholesky of the symmetrized 4x4 (s x s used) a into g; 1-based failing pivot
-BGS_DEV int chol4(const double (&a)[16], int s, double (&g)[16]) {
-#pragma unroll
-  for (int k = 0; k < 16; ++k) g[k] = 0.0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int i = 0; i <= j; ++i) {
-      if (j < s) {
-        double acc = 0.5 * (a[i + 4 * j] + a[j + 4 * i]);
-#pragma unroll
-        for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * g[k + 4 * j];
-        if (i == j) {
-          if (!(acc > 0.0)) return j + 1;
-          g[j + 4 * j] = sqrt(acc);
-        } else {
-          g[i + 4 * j] = acc / g[i + 4 * i];
-        }
-      }
+// (left, right) staged columns of product e: packed upper Y^T Y (10), full Y^T Z (16),
+// packed upper Z^T Z (10); columns 0..3 are Y, 4..7 are Z
+BGS_DEV void product_cols(int e, int& cu, int& cv) {
+  const bool zz = e >= 26;
+  if (e >= 10 && e < 26) {
+    cu = (e - 10) & 3;
+    cv = 4 + ((e - 10) >> 2);
+    return;
+  }
+  const int f = zz ? e - 26 : e;  // f = j (j + 1) / 2 + i, i <= j
+  const int j = f >= 6 ? 3 : f >= 3 ? 2 : f >= 1 ? 1 : 0;
+  const int i = f - j * (j + 1) / 2;
+  cu = i + (zz ? 4 : 0);
+  cv = j + (zz ? 4 : 0);
+}
+
+// Upper Cholesky of the symmetrized s x s block a (column-major 4 x 4) into g (shared),
+// on lanes 0..3 of one warp; every lane returns the same 1-based failing pivot (0 = ok).
+// Entry (i, j) = (0.5 (a_ij + a_ji) - sum_{k<i} g_ki g_kj) / g_ii, diagonal by sqrt --
+// the chol_serial expression; rows are finished in order, so the first failing pivot is
+// the same as in the column-ordered loop.
+BGS_DEV int chol4_lanes(const double* a, int s, double* g, int lane) {
+  if (lane < 16) g[lane] = 0.0;
+  __syncwarp();
+  for (int i = 0; i < s; ++i) {
+    double d = 0.0;
+    if (lane == i) {
+      double acc = 0.5 * (a[i + 4 * i] + a[i + 4 * i]);
+      for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * g[k + 4 * i];
+      d = acc;
     }
+    d = __shfl_sync(0xffffffffu, d, i);
+    if (!(d > 0.0)) return i + 1;
+    const double gii = sqrt(d);
+    if (lane > i && lane < s) {
+      const int j = lane;
+      double acc = 0.5 * (a[i + 4 * j] + a[j + 4 * i]);
+      for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * g[k + 4 * j];
+      g[i + 4 * j] = acc / gii;
+    }
+    if (lane == i) g[i + 4 * i] = gii;
+    __syncwarp();
   }
   return 0;
 }
 
-// w = g^{-T} b (g upper); 1-based index of a zero diagonal entry, else 0
-BGS_DEV int trsm4(const double (&g)[16], const double (&b)[16], int s, double (&w)[16]) {
-#pragma unroll
-  for (int k = 0; k < 16; ++k) w[k] = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i < s) {
-      const double gii = g[i + 4 * i];
-      if (gii == 0.0) return i + 1;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j < s) {
-          double acc = b[i + 4 * j];
-#pragma unroll
-          for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * w[k + 4 * j];
-          w[i + 4 * j] = acc / gii;
-        }
-      }
+// w = g^{-T} b (g upper, shared) column-parallel: lane j < s solves column j into w
+// (shared); every lane returns the same 1-based index of a zero diagonal (0 = ok).
+BGS_DEV int trsm4_lanes(const double* g, const double* b, int s, double* w, int lane) {
+  for (int i = 0; i < s; ++i)
+    if (g[i + 4 * i] == 0.0) return i + 1;
+  if (lane < 16) w[lane] = 0.0;
+  __syncwarp();
+  if (lane < s) {
+    const int j = lane;
+    for (int i = 0; i < s; ++i) {
+      double acc = b[i + 4 * j];
+      for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * w[k + 4 * j];
+      w[i + 4 * j] = acc / g[i + 4 * i];
     }
   }
+  __syncwarp();
   return 0;
 }
 }  // namespace
 
-__device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
-  const int s = p.s, kp = p.kp, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef BGS_STEP_STAMPS
+__device__ unsigned long long g_st_min = ~0ull, g_st_red = 0ull, g_st[8];
+BGS_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STAMP(i) \
+  if (threadIdx.x == 0) g_st[i] = gtime();
+#else
+#define STAMP(i)
+#endif
+
+__device__ __forceinline__ void onesync_step4_body(const SmallParams& p) {
+  const int s = p.s, kp = p.kp, tid = threadIdx.x, lane = tid & 31;
   const int nz = p.has_next ? s : 0;  // Z columns present
-  __shared__ double red[kStepThreads / 32][36];
+  __shared__ double yz[8 * kYZLd];    // [Y | Z] rows 0..kp, column stride kYZLd
+  __shared__ double part[36][kStepChunks];
   __shared__ double prod[36];
   __shared__ double blk[3][16];  // Omega = G[kp:, 0:s], P = G[kp:, s:2s], T = G[kp+s:, s:2s]
+  __shared__ double f_in[16], f_yd[16], f_s2[16], f_sd[16], f_sdp[16];  // s x s blocks (4 x 4)
   __shared__ int bad_flag;
   if (tid == 0) bad_flag = 0;
+  if (tid < 16) {
+    const int i = tid & 3, j = tid >> 2;
+    f_sdp[tid] = (i < s && j < s) ? p.sdiag[i + s * j] : 0.0;
+  }
   // previous S_diag (broadcast loads) and the status word, issued together
   double sdp[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) sdp[e] = ((e & 3) < s && (e >> 2) < s) ? p.sdiag[(e & 3) + s * (e >> 2)] : 0.0;
   const bool dead = status_bad(p.status);
-  if (tid < 48) {  // the s x s blocks thread 0 needs later, loaded now in parallel
+  if (tid < 48) {  // the s x s blocks warp 0 needs later, loaded now in parallel
     const int b = tid >> 4, e = tid & 15, i = e & 3, j = e >> 2;
     double v = 0.0;
     if (i < s && j < s && (b == 0 || p.has_next)) {
@@ -400,48 +449,33 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
     }
     blk[b][e] = v;
   }
-  // ---- one pass over rows: products, R column, scol_next copy, non-finite check ----
-  double acc[36];
-#pragma unroll
-  for (int e = 0; e < 36; ++e) acc[e] = 0.0;
+  // ---- 1. one pass over rows: stage [Y | Z], R column, scol_next copy, non-finite check ----
   int bad = 0;
   double rcol[2][4];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int r = tid + h * kStepThreads;
-    double y[4] = {0.0, 0.0, 0.0, 0.0}, z[4] = {0.0, 0.0, 0.0, 0.0};
     if (r < kp) {
+      double y[4] = {0.0, 0.0, 0.0, 0.0}, z[4] = {0.0, 0.0, 0.0, 0.0}, sp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         if (l < s) y[l] = p.G[r + (size_t)l * p.ldg];
         if (l < nz) z[l] = p.G[r + (size_t)(s + l) * p.ldg];
+        if (l < s) sp[l] = p.scol_prev[r + (size_t)l * p.ld_scol_prev];
       }
 #pragma unroll
-      for (int l = 0; l < 4; ++l) bad |= !isfinite(y[l]) | !isfinite(z[l]);
-#pragma unroll
       for (int l = 0; l < 4; ++l) {
+        bad |= !isfinite(y[l]) | !isfinite(z[l]);
+        yz[l * kYZLd + r] = y[l];
+        yz[(4 + l) * kYZLd + r] = z[l];
         // R(r, kp + l) = S_prev(r, l) + sum_m Y(r, m) S_diag(m, l)
         double a = 0.0;
 #pragma unroll
         for (int m2 = 0; m2 < 4; ++m2) a += y[m2] * sdp[m2 + 4 * l];
-        rcol[h][l] = l < s ? p.scol_prev[r + (size_t)l * p.ld_scol_prev] + a : 0.0;
+        rcol[h][l] = l < s ? sp[l] + a : 0.0;
         if (l < nz) p.scol_next[r + (size_t)l * p.ld_scol_next] = z[l];
       }
     }
-    // packed upper YtY (10), full YtZ (16), upper ZtZ (10)
-    int e = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i <= j; ++i, ++e) acc[e] = fma(y[i], y[j], acc[e]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i < 4; ++i, ++e) acc[e] = fma(y[i], z[j], acc[e]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i <= j; ++i, ++e) acc[e] = fma(z[i], z[j], acc[e]);
   }
   // the rest of the reduced Gram, for the non-finite check (rows kp..gm)
   for (int e = tid; e < (p.gm - kp) * p.gn; e += kStepThreads) {
@@ -449,21 +483,9 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
     bad |= !isfinite(p.G[r + (size_t)c * p.ldg]);
   }
   if (bad) atomicOr(&bad_flag, 1);
-#pragma unroll
-  for (int e = 0; e < 36; ++e) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-  }
-  if (lane == 0)
-#pragma unroll
-    for (int e = 0; e < 36; ++e) red[warp][e] = acc[e];
   __syncthreads();
+  STAMP(2)
   if (dead) return;
-  if (tid < 36) {
-    double t = 0.0;
-    for (int w = 0; w < kStepThreads / 32; ++w) t += red[w][tid];
-    prod[tid] = t;
-  }
   if (bad_flag) {
     if (tid == 0) set_status(p.status, ST_NON_FINITE, 0, p.k + 1, SITE_NONE, 0);
     return;
@@ -476,96 +498,112 @@ __device__ __noinline__ void onesync_step4_body(const SmallParams& p) {
       for (int l = 0; l < 4; ++l)
         if (l < s) p.R[r + (size_t)(kp + l) * p.ldr] = rcol[h][l];
   }
-  __syncthreads();
-  if (tid != 0) return;
-  // ---- thread 0: s x s factors in registers (the s x s Gram blocks come from blk) ----
-  double ytz[16], c[16], yd[16], sd[16];
-  {
-    int e = 0;
-    double yty[16];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i <= j; ++i) {
-        yty[i + 4 * j] = yty[j + 4 * i] = prod[e];
-        ++e;
-      }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ytz[i + 4 * j] = prod[e++];
-    // Y_diag = chol(Omega - Y^T Y)  (bcgs.cpp:321-327)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        c[i + 4 * j] = (i < s && j < s) ? blk[0][i + 4 * j] - yty[i + 4 * j] : 0.0;
+  // ---- 2. the 36 products over 7 row chunks (fixed order) ----
+  if (tid < 36 * kStepChunks) {
+    const int e = tid % 36, c = tid / 36;
+    int cu, cv;
+    product_cols(e, cu, cv);
+    const int len = (kp + kStepChunks - 1) / kStepChunks;
+    const int r0 = c * len, r1 = min(kp, r0 + len);
+    const double* u = yz + cu * kYZLd;
+    const double* v = yz + cv * kYZLd;
+    double a0 = 0.0, a1 = 0.0;
+    int r = r0;
+    for (; r + 1 < r1; r += 2) {
+      a0 = fma(u[r], v[r], a0);
+      a1 = fma(u[r + 1], v[r + 1], a1);
+    }
+    if (r < r1) a0 = fma(u[r], v[r], a0);
+    part[e][c] = a0 + a1;
   }
-  int piv = chol4(c, s, yd);
+  __syncthreads();
+  STAMP(3)
+  if (tid >= 32) return;
+  for (int e = lane; e < 36; e += 32) {  // lanes 0..3 also take products 32..35
+    double t = 0.0;
+#pragma unroll
+    for (int c = 0; c < kStepChunks; ++c) t += part[e][c];
+    prod[e] = t;
+  }
+  __syncwarp();
+  // ---- 3. warp 0: s x s factors, lane j owning column j ----
+  // Y_diag = chol(Omega - Y^T Y)  (bcgs.cpp:321-327)
+  if (lane < 16) {
+    const int i = lane & 3, j = lane >> 2;
+    const int lo = min(i, j), hi = max(i, j);
+    const double yty = prod[hi * (hi + 1) / 2 + lo];
+    f_in[lane] = (i < s && j < s) ? blk[0][lane] - yty : 0.0;
+  }
+  __syncwarp();
+  int piv = chol4_lanes(f_in, s, f_yd, lane);
+  STAMP(4)
   if (piv) {
-    set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
+    if (lane == 0) set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
     return;
   }
-#pragma unroll
-  for (int e = 0; e < 16; ++e)
-    if ((e & 3) < s && (e >> 2) < s) p.ydiag[(e & 3) + s * (e >> 2)] = yd[e];
-  // R_kk = upper_product(Y_diag, S_diag)  (bcgs.cpp:35-49, 333)
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (i < s && j < s) {
-        double a = 0.0;
-        if (i <= j)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k >= i && k <= j) a += yd[i + 4 * k] * sdp[k + 4 * j];
-        p.R[(kp + i) + (size_t)(kp + j) * p.ldr] = i <= j ? a : 0.0;
-      }
+  if (lane < 16) {
+    const int i = lane & 3, j = lane >> 2;
+    if (i < s && j < s) {
+      p.ydiag[i + s * j] = f_yd[lane];
+      // R_kk = upper_product(Y_diag, S_diag)  (bcgs.cpp:35-49, 333)
+      double a = 0.0;
+      if (i <= j)
+        for (int k = i; k <= j; ++k) a += f_yd[i + 4 * k] * f_sdp[k + 4 * j];
+      p.R[(kp + i) + (size_t)(kp + j) * p.ldr] = i <= j ? a : 0.0;
     }
+  }
   if (!p.has_next) return;
   // S2 = Y_diag^{-T} (P - Y^T Z); scol_next = [Z; S2]  (bcgs.cpp:336-344)
-  double bm[16], s2[16];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      bm[i + 4 * j] = (i < s && j < s) ? blk[1][i + 4 * j] - ytz[i + 4 * j] : 0.0;
-  piv = trsm4(yd, bm, s, s2);
+  if (lane < 16) {
+    const int i = lane & 3, j = lane >> 2;
+    f_in[lane] = (i < s && j < s) ? blk[1][lane] - prod[10 + lane] : 0.0;
+  }
+  __syncwarp();
+  piv = trsm4_lanes(f_yd, f_in, s, f_s2, lane);
+  STAMP(5)
   if (piv) {
-    set_status(p.status, ST_SINGULAR, piv, p.k + 1, SITE_NONE, 0);
+    if (lane == 0) set_status(p.status, ST_SINGULAR, piv, p.k + 1, SITE_NONE, 0);
     return;
   }
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < s && j < s) p.scol_next[(kp + i) + (size_t)j * p.ld_scol_next] = s2[i + 4 * j];
+  if (lane < 16) {
+    const int i = lane & 3, j = lane >> 2;
+    if (i < s && j < s) p.scol_next[(kp + i) + (size_t)j * p.ld_scol_next] = f_s2[lane];
+  }
   if (p.os_mode == OS_PYTH) {
     // S_diag = chol(T - scol^T scol), scol^T scol = Z^T Z + S2^T S2  (bcgs.cpp:352-359)
-    double t[16];
-    int e = 26;
+    __syncwarp();
+    if (lane < 16) {
+      const int i = lane & 3, j = lane >> 2;
+      const int lo = min(i, j), hi = max(i, j);
+      double a = prod[26 + hi * (hi + 1) / 2 + lo];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int i = 0; i <= j; ++i) {
-        double a = prod[e++];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) a += s2[k + 4 * i] * s2[k + 4 * j];
-        const double v = (i < s && j < s) ? blk[2][i + 4 * j] : 0.0;
-        const double vt = (i < s && j < s) ? blk[2][j + 4 * i] : 0.0;
-        t[i + 4 * j] = v - a;
-        t[j + 4 * i] = vt - a;
-      }
-    piv = chol4(t, s, sd);
-    if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 2, SITE_FIRST_PASS, p.kappa_power);
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if ((k & 3) < s && (k >> 2) < s) p.sdiag[(k & 3) + s * (k >> 2)] = sd[k];
+      for (int k = 0; k < 4; ++k) a += f_s2[k + 4 * lo] * f_s2[k + 4 * hi];
+      f_in[lane] = ((i < s && j < s) ? blk[2][lane] : 0.0) - a;
+    }
+    __syncwarp();
+    piv = chol4_lanes(f_in, s, f_sd, lane);
+    if (piv && lane == 0) set_status(p.status, ST_NOT_SPD, piv, p.k + 2, SITE_FIRST_PASS, p.kappa_power);
+    __syncwarp();
+    if (lane < 16) {
+      const int i = lane & 3, j = lane >> 2;
+      if (i < s && j < s) p.sdiag[i + s * j] = f_sd[lane];
+    }
+#ifdef BGS_STEP_STAMPS
+    STAMP(6)
+    if (tid == 0 && kp % 40 == 0)
+      printf("[step stamps] kp %d: reduce %llu | last-detect %llu | pass %llu | products %llu | chol %llu | trsm %llu | chol2+stores %llu ns (entry->end %llu)\n",
+             kp, g_st_red - g_st_min, g_st[1] - g_st_red, g_st[2] - g_st[1], g_st[3] - g_st[2], g_st[4] - g_st[3],
+             g_st[5] - g_st[4], g_st[6] - g_st[5], g_st[6] - g_st_min);
+    if (tid == 0) {
+      g_st_min = ~0ull;
+      g_st_red = 0ull;
+    }
+#endif
   } else if (p.os_mode == OS_SKIP) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if ((k & 3) < s && (k >> 2) < s) p.sdiag[(k & 3) + s * (k >> 2)] = (k & 3) == (k >> 2) ? 1.0 : 0.0;
+    if (lane < 16) {
+      const int i = lane & 3, j = lane >> 2;
+      if (i < s && j < s) p.sdiag[i + s * j] = i == j ? 1.0 : 0.0;
+    }
   }
 }
 
@@ -578,9 +616,19 @@ __global__ void __launch_bounds__(kStepThreads, 1) onesync_step4_kernel(SmallPar
 // Gram (the threadfence-reduction pattern); it also re-arms the ticket for the next launch.
 static_assert(RED_THREADS == kStepThreads, "one block shape for both halves");
 __global__ void __launch_bounds__(kStepThreads, 1)
-    reduce_step4_kernel(const ReduceArgs r, SmallParams p, unsigned* ticket) {
+    reduce_step4_kernel(const ReduceArgs r, int nblk, SmallParams p, unsigned* ticket) {
   __shared__ int last;
-  gram_reduce_body(r);
+#ifdef BGS_STEP_STAMPS
+  const unsigned long long t_in = gtime();
+#endif
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) gram_reduce_body(r, b);
+#ifdef BGS_STEP_STAMPS
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMin(&g_st_min, t_in);
+    atomicMax(&g_st_red, gtime());
+  }
+#endif
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -588,6 +636,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   if (!last) return;
   __threadfence();
   if (threadIdx.x == 0) *ticket = 0u;
+  STAMP(1)
   onesync_step4_body(p);
 }
 
@@ -596,10 +645,12 @@ bool small_mergeable(const SmallParams& p) {
 }
 
 cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallParams& p,
-                                unsigned* ticket, cudaStream_t st, int* launches) {
+                                unsigned* ticket, int sms, cudaStream_t st, int* launches) {
   if (!small_mergeable(p)) return cudaErrorInvalidValue;
-  reduce_step4_kernel<<<(entries + RED_ENTRIES - 1) / RED_ENTRIES, kStepThreads, 0, st>>>(r, p,
-                                                                                        ticket);
+  // one wave: the step body needs ~140 registers, so one CTA per SM; extra entry blocks
+  // are looped over inside the CTA instead of running as a second wave
+  const int nblk = (entries + RED_ENTRIES - 1) / RED_ENTRIES;
+  reduce_step4_kernel<<<std::min(nblk, sms), kStepThreads, 0, st>>>(r, nblk, p, ticket);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
