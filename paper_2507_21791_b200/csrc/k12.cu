@@ -53,8 +53,8 @@ constexpr int kConsWarps = kGroups * kGroupWarps;  // warps 0-7: two consumer gr
 constexpr int kProdWarp = kConsWarps;              // warp 8: TMA producer (warps 8-11: its warpgroup)
 constexpr int kThreads = 32 * (kConsWarps + 4);
 // setmaxnreg: the producer warpgroup gives registers to the two consumer warpgroups
-// (4 x 32 x (2 x 232 + 40) = 64512 <= 65536)
-constexpr int kProdRegs = 40, kConsRegs = 232;
+// (4 x 32 x (2 x 240 + 24) = 64512 <= 65536)
+constexpr int kProdRegs = 24, kConsRegs = 240;
 constexpr int kChunkRows = 32;
 constexpr int kUnitChunkBytes = 8 * kChunkRows * 8;  // one 8-column unit of one 32-row chunk
 constexpr int kRedBytes = kGroups * kGroupWarps * 4 * 32 * 16;  // [group][warp][m-tile][lane]
@@ -579,6 +579,9 @@ bool k12_plan(SplitParams& p) {
     if (!S) continue;
     q.kw = kw_t;
     q.mtw = mtw_for(kw_t, cd.R);
+    // one narrower instance: KW = 16 at R = 1 would carry MTW = 9 (folds every stage,
+    // spills) where 8 tiles per warp suffice (kp = 244..252 at s = 4)
+    if (cd.R == 1 && kw_t == 16 && mtw <= 8) q.mtw = 8;
     q.stages = S;
     p = q;
     static const bool verbose = getenv("BGS_K12C_VERBOSE") != nullptr;
@@ -590,9 +593,8 @@ bool k12_plan(SplitParams& p) {
   return false;
 }
 
-template <int KW, int R>
+template <int KW, int R, int MTW = mtw_for(KW, R)>
 static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
-  constexpr int MTW = mtw_for(KW, R);
   auto k = k12_kernel<KW, MTW, R>;
   const size_t smem = k12_smem_bytes(p.stages, p.slot_units, R, p.cluster);
   cudaError_t e = ensure_smem(k, smem);
@@ -614,6 +616,7 @@ static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
 
 template <int R>
 static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
+  if (R == 1 && p.kw == 16 && p.mtw == 8) return launch_k12<16, 1, 8>(p, grid, st);
   switch (p.kw) {
 #define BGS_KW(K) \
   case K: return launch_k12<K, R>(p, grid, st);
