@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--config", type=int, default=0, choices=[0, 1, 2, 5],
                     help="BASELINE.json preset: 1 (n=1e5 m=64), 2 (n=1e6 m=400, the default "
                          "workload), 5 (n=1e7 m=400 geometric kappa=1e6)")
+    ap.add_argument("--nccl", action="store_true",
+                    help="N=1: run the collective path on a one-rank NCCL communicator")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -77,6 +79,8 @@ def workload_config(a, world):
         "variant": a.variant, "n": a.n, "m": a.m, "s": a.s, "seed": a.seed,
         "dist": a.dist, **({"kappa": a.kappa} if a.dist == "geometric" else {}),
         "parallelism": f"row-sharded dp{world} (1-D ceil split), 1 allreduce per block step",
+        "collectives": ("NCCL" if world > 1 or getattr(a, "nccl", False)
+                        else "none (one GPU: in-kernel reduction)"),
         "l2": f"inputs exceed L2: X is {a.n * a.m * 8 / 1e9:.2f} GB (126 MB L2), no flush needed",
     }
 
@@ -269,6 +273,8 @@ def run_ours(a):
         obj = [bgs.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    elif a.nccl:
+        uid = bgs.nccl_unique_id()
     ctx = bgs.Context(local, rank, world, uid)
     v = int(bgs.parse_variant(a.variant))
     n, m, s = a.n, a.m, a.s

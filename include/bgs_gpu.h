@@ -87,8 +87,10 @@ int bgs_shard_rows(long n, int procs, int rank, long* row0, long* rows); /* dist
 
 /* ---- context: device, stream, NCCL communicator, workspaces -----------------------
  * Replaces Communicator + run_spmd's per-rank setup (communicator.hpp:50-152).
- * nranks == 1: single GPU, no NCCL.  nranks > 1: one process (or thread) per GPU;
- * nccl_unique_id points to the 128-byte ncclUniqueId shared by all ranks. */
+ * nranks == 1: single GPU, no NCCL unless nccl_unique_id is non-null (then a one-rank
+ * communicator carries the same collectives as the multi-GPU path).  nranks > 1: one
+ * process (or thread) per GPU; nccl_unique_id points to the 128-byte ncclUniqueId shared
+ * by all ranks. */
 int bgs_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
                    bgs_ctx** out, bgs_error* err);
 void bgs_ctx_destroy(bgs_ctx* ctx);

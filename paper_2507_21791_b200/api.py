@@ -292,7 +292,8 @@ class FactorOutcome:
 
 
 class Context:
-    """A device + stream (+ NCCL communicator when nranks > 1) + workspaces."""
+    """A device + stream (+ NCCL communicator when nranks > 1, or when an id is given for a
+    one-rank context) + workspaces."""
 
     def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1,
                  nccl_unique_id: Optional[bytes] = None):

@@ -1492,7 +1492,9 @@ int bgs_ctx_create(int device, int rank, int nranks, const void* uid, bgs_ctx** 
     CUDA_OK(cudaEventCreate(&c->e0));
     CUDA_OK(cudaEventCreate(&c->e1));
     CUDA_OK(cudaEventCreateWithFlags(&c->entry, cudaEventDisableTiming));
-    if (nranks > 1) {
+    // an NCCL communicator for every multi-rank context, and for a one-rank context
+    // whose caller passes an id (the collective path on one GPU: tests, bring-up)
+    if (nranks > 1 || uid) {
       if (!uid) fail(BGS_E_COLLECTIVE, "nranks > 1 needs an ncclUniqueId");
       if (!nccl().ok) fail(BGS_E_COLLECTIVE, "libnccl.so.2 could not be loaded");
       ncclUniqueId id;
@@ -1662,7 +1664,7 @@ int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0
     if (ldx < n_local || ldq < n_local || ldr < m) fail(BGS_E_DIMENSION, "leading dimension too small");
     select_device(c);
     order_after_caller(c);
-    Runner run(c, variant, n, m, s, c->nranks, c->nranks > 1, stats);
+    Runner run(c, variant, n, m, s, c->nranks, c->comm != nullptr, stats);
     Shard sh;
     sh.row0 = row0;
     sh.rows = n_local;
@@ -1757,7 +1759,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
     (void)n;
     const int si = 8;
     // Q^T Q in panels of 8 right columns through K1 (+ NCCL allreduce)
-    Runner run(c, BGS_BCGSI_PLUS_P_1S, std::max(n, m), m, 1, c->nranks, c->nranks > 1, nullptr);
+    Runner run(c, BGS_BCGSI_PLUS_P_1S, std::max(n, m), m, 1, c->nranks, c->comm != nullptr, nullptr);
     Shard sh;
     sh.rows = n_local;
     sh.X = d_x; sh.ldx = ldx;
@@ -1824,7 +1826,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
                               m, cudaMemcpyHostToDevice, c->stream));
     CUDA_OK(residual_launch(d_x, ldx, d_q, ldq, dr.d(), m, n_local, m, 1.0, 1.0, c->metrics.d(),
                             out2, c->sms, c->stream));
-    if (c->nranks > 1)
+    if (c->comm)
       NCCL_OK(nccl().AllReduce(out2, out2, 2, ncclDouble, ncclSum, c->comm, c->stream));
     double h[2];
     CUDA_OK(cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, c->stream));

@@ -467,3 +467,33 @@ def test_config5_full_size_orthogonality_loss(gpu_ctx):
     assert loo < 1e-13 and res < 1e-14, (loo, res)
     del X, Q
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------------------------------
+# The multi-GPU code path on one GPU: a one-rank NCCL communicator
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("v", VARIANTS)
+def test_nccl_path_on_one_rank_matches_local_path(oracle, gpu_ctx, v):
+    """A context built with an ncclUniqueId runs the collective path (ncclAllReduce of every
+    Gram, the NCCL group of allgather(R roots) + fused-Gram allreduce in every TSQR, the
+    standalone reduce and step launches) on a one-rank communicator.  With one rank each
+    collective is an identity, so Q and R must equal the local path's bit for bit, and
+    the sync accounting must not change."""
+    import torch
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 30000, 48, 4
+    x = oracle.gen_matrix(n, m, s, 1.0, 777, True)
+    ld = (n + 31) // 32 * 32
+    X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    X[:, :n] = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    outs = []
+    for ctx in (gpu_ctx, bgs.Context(0, 0, 1, bgs.nccl_unique_id())):
+        Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+        r, st, tm = bgs.factor_device(ctx, v, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+        torch.cuda.synchronize()
+        outs.append((Q[:, :n].cpu().numpy(), r, st.sync_count, st.words_reduced, st.event_labels))
+    (q0, r0, c0, w0, l0), (q1, r1, c1, w1, l1) = outs
+    assert (c0, w0, l0) == (c1, w1, l1)
+    assert np.array_equal(r0, r1) and np.array_equal(q0, q1)
+    ref = oracle.factor(v, x, s, 1, metrics=False)
+    assert_r_close(r1, ref.r)
