@@ -570,8 +570,15 @@ bool k12_plan(SplitParams& p) {
     if (kw_t > kw_max) continue;
     const char* me = getenv("BGS_K12C_MINS");  // experiments: minimum ring depth (default 3)
     const int min_s = me ? std::max(2, atoi(me)) : 3;
+    // Ring depth: deeper is not better.  Measured per step at config 2 (S = 2..8,
+    // profiles/r01_stage_depth.log): the CTA-pair plans and the one-CTA R = 1 plans with
+    // >= 6 output tiles per warp run 2-7% faster with 3 stages than with 4+; the taller
+    // early stages (R = 2, 4) want 4.  BGS_K12C_MAXS overrides (experiments).
+    const int depth = (cd.C == 2 || (cd.R == 1 && mtw_for(kw_t, cd.R) >= 6)) ? 3 : 4;
+    const char* xe = getenv("BGS_K12C_MAXS");
+    const int max_s = std::max(min_s, xe ? std::min(kMaxStages, atoi(xe)) : depth);
     int S = 0;
-    for (int st = kMaxStages; st >= min_s; --st)
+    for (int st = max_s; st >= min_s; --st)
       if (k12_smem_bytes(st, q.slot_units, cd.R, cd.C) + kStaticSmem + 256 <= (size_t)kSmemOptin) {
         S = st;
         break;
