@@ -864,12 +864,6 @@ class Runner {
     p.R = c->R.d();
     p.ldr = (int)m;
     p.status = status;
-    static const int exp_skip = getenv("BGS_EXP_SKIP_SMALL") ? atoi(getenv("BGS_EXP_SKIP_SMALL")) : 0;
-    if (exp_skip && pend.on && small_mergeable(p)) {  // TEMP experiment: 1 = skip both, 2 = reduce only
-      pend.on = false;
-      if (exp_skip == 2) CUDA_OK(gram_reduce_launch_args(pend.a, pend.entries, c->stream, &c->launches));
-      return;
-    }
     if (pend.on && small_mergeable(p)) {
       pend.on = false;
       Prof pr(c, "reduce_small", pend.bytes, 0.0);

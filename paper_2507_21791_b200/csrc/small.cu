@@ -450,37 +450,48 @@ __device__ __forceinline__ void onesync_step4_body(const SmallParams& p) {
     blk[b][e] = v;
   }
   // ---- 1. one pass over rows: stage [Y | Z], R column, scol_next copy, non-finite check ----
-  int bad = 0;
+  // Every load of the pass is issued before the first store (one L2 round trip: the
+  // stores to scol_next could alias G as far as the compiler knows).
+  double y[2][4], z[2][4], sp[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = tid + h * kStepThreads;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      y[h][l] = (r < kp && l < s) ? p.G[r + (size_t)l * p.ldg] : 0.0;
+      z[h][l] = (r < kp && l < nz) ? p.G[r + (size_t)(s + l) * p.ldg] : 0.0;
+      sp[h][l] = (r < kp && l < s) ? p.scol_prev[r + (size_t)l * p.ld_scol_prev] : 0.0;
+    }
+  }
+  // the rest of the reduced Gram, for the non-finite check (rows kp..gm)
+  const int tail = (p.gm - kp) * p.gn;
+  const double tv = tid < tail ? p.G[kp + tid % (p.gm - kp) + (size_t)(tid / (p.gm - kp)) * p.ldg] : 0.0;
+  int bad = !isfinite(tv);
+  for (int e = tid + kStepThreads; e < tail; e += kStepThreads) {
+    const int r = kp + e % (p.gm - kp), c = e / (p.gm - kp);
+    bad |= !isfinite(p.G[r + (size_t)c * p.ldg]);
+  }
   double rcol[2][4];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int r = tid + h * kStepThreads;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      bad |= !isfinite(y[h][l]) | !isfinite(z[h][l]);
+      // R(r, kp + l) = S_prev(r, l) + sum_m Y(r, m) S_diag(m, l)
+      double a = 0.0;
+#pragma unroll
+      for (int m2 = 0; m2 < 4; ++m2) a += y[h][m2] * sdp[m2 + 4 * l];
+      rcol[h][l] = l < s ? sp[h][l] + a : 0.0;
+    }
     if (r < kp) {
-      double y[4] = {0.0, 0.0, 0.0, 0.0}, z[4] = {0.0, 0.0, 0.0, 0.0}, sp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
-        if (l < s) y[l] = p.G[r + (size_t)l * p.ldg];
-        if (l < nz) z[l] = p.G[r + (size_t)(s + l) * p.ldg];
-        if (l < s) sp[l] = p.scol_prev[r + (size_t)l * p.ld_scol_prev];
-      }
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        bad |= !isfinite(y[l]) | !isfinite(z[l]);
-        yz[l * kYZLd + r] = y[l];
-        yz[(4 + l) * kYZLd + r] = z[l];
-        // R(r, kp + l) = S_prev(r, l) + sum_m Y(r, m) S_diag(m, l)
-        double a = 0.0;
-#pragma unroll
-        for (int m2 = 0; m2 < 4; ++m2) a += y[m2] * sdp[m2 + 4 * l];
-        rcol[h][l] = l < s ? sp[l] + a : 0.0;
-        if (l < nz) p.scol_next[r + (size_t)l * p.ld_scol_next] = z[l];
+        yz[l * kYZLd + r] = y[h][l];
+        yz[(4 + l) * kYZLd + r] = z[h][l];
+        if (l < nz) p.scol_next[r + (size_t)l * p.ld_scol_next] = z[h][l];
       }
     }
-  }
-  // the rest of the reduced Gram, for the non-finite check (rows kp..gm)
-  for (int e = tid; e < (p.gm - kp) * p.gn; e += kStepThreads) {
-    const int r = kp + e % (p.gm - kp), c = e / (p.gm - kp);
-    bad |= !isfinite(p.G[r + (size_t)c * p.ldg]);
   }
   if (bad) atomicOr(&bad_flag, 1);
   __syncthreads();
