@@ -214,6 +214,44 @@ def test_non_finite_input_raises(gpu_ctx):
         bgs.run_factor(3, x, 4, 1, metrics=False)
 
 
+@pytest.mark.parametrize("v", VARIANTS, ids=lambda v: NAMES[v])
+def test_zero_matrix_outcome_matches_oracle(oracle, gpu_ctx, v):
+    """X = 0 (the reference's x_was_zero case): every variant ends the way the reference
+    does -- BCGSI+ completes (R = 0), BCGSPIPI+ aborts NotSpd at its first-pass
+    normalization, the one-sync variants hit a zero on R's diagonal (SingularError)."""
+    import paper_2507_21791_b200 as bgs
+    x = np.zeros((64, 8), order="F")
+    ref = oracle.factor(v, x, 2, 1, metrics=False)
+    if ref.rc == 0:
+        out = bgs.run_factor(v, x, 2, 1, metrics=True)
+        assert out.ok and out.x_was_zero
+        assert np.array_equal(out.r, ref.r)
+        assert out.stats.sync_count == ref.sync_count
+    elif ref.rc == 2:
+        out = bgs.run_factor(v, x, 2, 1, metrics=False)
+        assert not out.ok and out.error.split(" (")[0] == ref.msg.split(" (")[0]
+    else:
+        with pytest.raises(bgs.api.SingularError):
+            bgs.run_factor(v, x, 2, 1, metrics=False)
+
+
+@pytest.mark.parametrize("v", VARIANTS, ids=lambda v: NAMES[v])
+@pytest.mark.parametrize("n,m,s", [(8, 8, 2), (16, 16, 4), (33, 32, 16), (5, 4, 1)])
+def test_square_and_minimal_shapes(oracle, gpu_ctx, v, n, m, s):
+    """n = m (and n = m + 1 with one wide block): the smallest shapes validate() admits."""
+    import paper_2507_21791_b200 as bgs
+    x = oracle.gen_matrix(n, m, s, 10.0, 4242, False)
+    ref = oracle.factor(v, x, s, 1, metrics=True)
+    if ref.rc != 0:
+        pytest.skip("oracle aborts on this input")
+    out = bgs.run_factor(v, x, s, 1, metrics=False)
+    assert out.ok, out.error
+    assert out.stats.sync_count == ref.sync_count
+    assert_structure(out.r)
+    assert_r_close(out.r, ref.r)
+    assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
+
+
 def test_malformed_inputs_rejected(gpu_ctx):
     import paper_2507_21791_b200 as bgs
     x = np.random.default_rng(2).standard_normal((16, 6))
