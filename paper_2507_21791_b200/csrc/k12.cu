@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     const uint32_t xb_local = smem_u32(xbuf);
     const uint32_t xfull_local = smem_u32(xfull);
     const bool prof = p.phase && gtid == 0;
+    // per-stage timeline of CTA 0 (both groups, first kTl group-stages): wait start, data
+    // ready, update done, exchange done, epilogue done, Gram done (BGS_TILE_PROF)
+    constexpr int kTl = 48;
+    unsigned long long* tl = (prof && blockIdx.x == 0) ? p.phase + 2560 + (size_t)g * kTl * 6 : nullptr;
     unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};  // full wait, update, exchange, epilogue, gram
     const unsigned long long t_begin = prof ? clock64() : 0;
     for (int j = 0;; ++j) {
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       mbar_wait(&full[slot], (it / S) & 1);
       unsigned long long t1 = prof ? clock64() : 0;
       if (prof) ph[0] += t1 - t0;
+      if (tl && j < kTl) { tl[j * 6 + 0] = t0; tl[j * 6 + 1] = t1; }
       const uint32_t base = sbase + (uint32_t)(slot * slot_bytes);
       const long row0 = (st0 + it) * RS;
       const int vrows = (int)((p.n_rows - row0) < RS ? (p.n_rows - row0) : RS);
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         for (int q = 0; q < 4; ++q) sts128(red_w + (uint32_t)(q * 32 * 16), d[q][0], d[q][1]);
       }
       bar_named(gbar, 32 * kGroupWarps);
-      if (prof) { const unsigned long long t = clock64(); ph[1] += t - t1; t1 = t; }
+      if (prof) { const unsigned long long t = clock64(); ph[1] += t - t1; t1 = t; if (tl && j < kTl) tl[j * 6 + 2] = t; }
 
       // ---- per chunk: sum the KS warp partials of this lane's row (fixed order) ----
       double D0[R], D1[R];
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
           D1[ch] += o.y;
         }
       }
-      if (prof) { const unsigned long long t = clock64(); ph[2] += t - t1; t1 = t; }
+      if (prof) { const unsigned long long t = clock64(); ph[2] += t - t1; t1 = t; if (tl && j < kTl) tl[j * 6 + 3] = t; }
 
       // ---- epilogue on the tensor core: [A | B] = [srcA - DA | srcB - DB] M ----
       // A operand lane (i, kk): z[row][kk] and z[row][4 + kk]; D[row][c] sits in lane
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         }
       }
       bar_named(gbar, 32 * kGroupWarps);
-      if (prof) { const unsigned long long t = clock64(); ph[3] += t - t1; t1 = t; }
+      if (prof) { const unsigned long long t = clock64(); ph[3] += t - t1; t1 = t; if (tl && j < kTl) tl[j * 6 + 4] = t; }
 
       // ---- Gram of this rank's output tiles (w + 4 jj) against span 1 ----
       // k-index kk of pass u covers chunk rows 16 (kk & 1) + 8 (kk >> 1) + 4u + {0..3}: for
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
       if ((j % kFold) == kFold - 1) fold();
-      if (prof) { const unsigned long long t = clock64(); ph[4] += t - t1; }
+      if (prof) { const unsigned long long t = clock64(); ph[4] += t - t1; if (tl && j < kTl) tl[j * 6 + 5] = t; }
     }
     fold();
     if (prof) {

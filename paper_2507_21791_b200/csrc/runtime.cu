@@ -1260,6 +1260,19 @@ class Runner {
               "exchange %.0f epilogue %.0f gram %.0f | total %.0f\n",
               kt[6], kt[0] / kt[6], kt[1] / kt[6], kt[2] / kt[6], kt[3] / kt[6], kt[4] / kt[6],
               kt[5] / kt[6]);
+    // K12c timeline of CTA 0 in the last profiled launch: [group][stage][6 stamps]
+    constexpr int kTl0 = 4096 + 2560;
+    if (getenv("BGS_TIMELINE") && h[kTl0] != 0) {
+      const unsigned long long base = std::min(h[kTl0], h[kTl0 + 48 * 6]);
+      for (int g = 0; g < 2; ++g)
+        for (int j = 0; j < 48; ++j) {
+          const unsigned long long* t = &h[kTl0 + (g * 48 + j) * 6];
+          if (!t[0]) continue;
+          fprintf(stderr, "[k12c timeline] g %d j %2d:", g, j);
+          for (int i = 0; i < 6; ++i) fprintf(stderr, " %llu", t[i] - base);
+          fprintf(stderr, "\n");
+        }
+    }
   }
 
   void run() {
