@@ -238,6 +238,12 @@ BGS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// programmatic dependent launch: wait for the preceding grid (its memory is visible
+// after this; returns at once when the launch was not programmatic) / allow the next
+// grid to launch early
+BGS_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+BGS_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // named barrier over `threads` threads (id 0 is __syncthreads)
 BGS_DEV void bar_named(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");

@@ -70,9 +70,33 @@ size_t k12_smem_bytes(int stages, int slot_units, int R, int C) {
          (C == 2 ? xchg_bytes(R) : 0) + (size_t)(2 * stages + 4) * sizeof(uint64_t);
 }
 
+#ifdef BGS_STEP_STAMPS
+// Debug builds (-DBGS_STEP_STAMPS, tools/stamp_run.py): %globaltimer of every CTA's entry
+// dependency-wait release, factors done and first stage ready: [step k][min, max] x 4
+__device__ unsigned long long g_k12_log[512 * 8];
+extern "C" int bgs_dbg_k12_stamps(unsigned long long* out, int reset) {
+  if (reset) {
+    static unsigned long long init[512 * 8];
+    for (int i = 0; i < 512 * 4; ++i) {
+      init[2 * i] = ~0ull;
+      init[2 * i + 1] = 0ull;
+    }
+    return (int)cudaMemcpyToSymbol(g_k12_log, init, sizeof init);
+  }
+  return (int)cudaMemcpyFromSymbol(out, g_k12_log, sizeof g_k12_log);
+}
+__device__ __forceinline__ unsigned long long k12_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int KW, int MTW, int R>
 __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant__ SplitParams p) {
-  if (p.status && status_bad(p.status)) return;  // both ranks read the same word
+#ifdef BGS_STEP_STAMPS
+  const unsigned long long t_entry = k12_gtime();
+#endif
   constexpr int KS = 4 / R;                     // k-split factor of the update
   constexpr int RS = kChunkRows * R;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -100,6 +124,11 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
   const long st0 = (long)cl * T / ncl;
   const int nst = (int)((long)(cl + 1) * T / ncl - st0);
   const int s = p.s;
+  // Launched as a programmatic dependent of the merged reduce + step kernel (p.pdl), the
+  // producer streams the first stages before the wait: X / Q were written by kernels that
+  // completed before that kernel started; only the coefficients and the status word are
+  // its outputs.
+  const int pre = p.pdl ? min(S, nst) : 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -108,51 +137,6 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     }
     for (int i = 0; i < 4; ++i) mbar_init(&xfull[i], 1);
     fence_mbar_init();
-  }
-  // Epilogue factors padded to 4x4 with identity: TA^{-1}, TB^{-1}, W = S2 TB^{-1}.
-  if (threadIdx.x < 16) {
-    const int i = threadIdx.x & 3, j = threadIdx.x >> 2;
-    const bool in = i < s && j < s;
-    const double id = i == j ? 1.0 : 0.0;
-    ep_t[0][threadIdx.x] = (in && p.TA) ? p.TA[i + j * s] : id;
-    ep_t[1][threadIdx.x] = (in && p.TB) ? p.TB[i + j * s] : id;
-    ep_s2[threadIdx.x] = (in && p.upd_a && p.upd_b) ? p.CB[p.kp + i + (size_t)j * p.ldcb] : 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    const int which = threadIdx.x >> 2, j = threadIdx.x & 3;
-    const double* Tm = ep_t[which];
-    double* Ti = which ? ep_bi : ep_ai;
-    for (int i = 3; i >= 0; --i) {  // column j of T^{-1}: T y = e_j
-      double acc = (i == j) ? 1.0 : 0.0;
-      for (int l = i + 1; l < 4; ++l) acc -= Tm[i + 4 * l] * Ti[l + 4 * j];
-      Ti[i + 4 * j] = acc / Tm[i + 4 * i];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 16) {
-    const int m = threadIdx.x & 3, j = threadIdx.x >> 2;
-    double acc = 0.0;
-    for (int l = 0; l < 4; ++l) acc += ep_s2[m + 4 * l] * ep_bi[l + 4 * j];
-    ep_w[m + 4 * j] = acc;
-  }
-  __syncthreads();
-  // M[l][j] (row-major 8 x 8): out = z M with z = [srcA - DA, srcB - DB]
-  if (threadIdx.x < 64) {
-    const int l = threadIdx.x >> 3, j = threadIdx.x & 7;
-    double v = 0.0;
-    if (l < 4 && j < 4) {
-      v = p.upd_a ? ep_ai[l + 4 * j] : 0.0;
-    } else if (l < 4) {  // -(TA^-1 W)[l][j-4]
-      if (p.upd_a && p.upd_b) {
-        double acc = 0.0;
-        for (int m = 0; m < 4; ++m) acc += ep_ai[l + 4 * m] * ep_w[m + 4 * (j - 4)];
-        v = -acc;
-      }
-    } else if (j >= 4) {
-      v = p.upd_b ? ep_bi[(l - 4) + 4 * (j - 4)] : 0.0;
-    }
-    ep_m[l * 8 + j] = v;
   }
   __syncthreads();
   if (pair) cluster_sync_all();  // the peer's mbarriers exist before any st.async reaches them
@@ -169,6 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       for (int i = 0; i < 2; ++i) prefetch_tmap(&p.map1[i]);
       const uint32_t bytes = (uint32_t)(nloc * R * kUnitChunkBytes);
       for (int it = 0; it < nst; ++it) {
+        if (it == pre) {
+          // the stages past the prefetch wait for the preceding kernel (its status word)
+          griddep_wait();
+          if (p.status && status_bad(p.status)) break;  // both ranks read the same word
+        }
         const int slot = it % S;
         if (it >= S) mbar_wait(&empty[slot], ((it / S) - 1) & 1);
         mbar_arrive_expect_tx(&full[slot], bytes);
@@ -203,7 +192,16 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     __syncwarp();
   } else {
     // ---------------- consumers: group g takes stages g, g+2, g+4, ... ----------------
+    // Coefficients, factors and the status word come from the preceding kernel.
+    griddep_wait();
+#ifdef BGS_STEP_STAMPS
+    const unsigned long long t_wait = k12_gtime();
+#endif
     const int g = warp / kGroupWarps, w = warp % kGroupWarps;
+    if (p.status && status_bad(p.status)) {
+      // an earlier step failed: drain the stages prefetched before the producer saw it
+      for (int it = g; it < pre; it += kGroups) mbar_wait(&full[it % S], (it / S) & 1);
+    } else {
     const int gtid = threadIdx.x - 32 * kGroupWarps * g;
     const int ii = lane >> 2, kk = lane & 3;
     const int gbar = 1 + g;
@@ -232,6 +230,53 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       }
       bco[t] = v;
     }
+    // (after the coefficient loads: their latency hides under the factor arithmetic)
+    // Epilogue factors padded to 4x4 with identity: TA^{-1}, TB^{-1}, W = S2 TB^{-1}.
+    if (threadIdx.x < 16) {
+      const int i = threadIdx.x & 3, j = threadIdx.x >> 2;
+      const bool in = i < s && j < s;
+      const double id = i == j ? 1.0 : 0.0;
+      ep_t[0][threadIdx.x] = (in && p.TA) ? p.TA[i + j * s] : id;
+      ep_t[1][threadIdx.x] = (in && p.TB) ? p.TB[i + j * s] : id;
+      ep_s2[threadIdx.x] = (in && p.upd_a && p.upd_b) ? p.CB[p.kp + i + (size_t)j * p.ldcb] : 0.0;
+    }
+    bar_named(5, 32 * kConsWarps);
+    if (threadIdx.x < 8) {
+      const int which = threadIdx.x >> 2, j = threadIdx.x & 3;
+      const double* Tm = ep_t[which];
+      double* Ti = which ? ep_bi : ep_ai;
+      for (int i = 3; i >= 0; --i) {  // column j of T^{-1}: T y = e_j
+        double acc = (i == j) ? 1.0 : 0.0;
+        for (int l = i + 1; l < 4; ++l) acc -= Tm[i + 4 * l] * Ti[l + 4 * j];
+        Ti[i + 4 * j] = acc / Tm[i + 4 * i];
+      }
+    }
+    bar_named(5, 32 * kConsWarps);
+    if (threadIdx.x < 16) {
+      const int m = threadIdx.x & 3, j = threadIdx.x >> 2;
+      double acc = 0.0;
+      for (int l = 0; l < 4; ++l) acc += ep_s2[m + 4 * l] * ep_bi[l + 4 * j];
+      ep_w[m + 4 * j] = acc;
+    }
+    bar_named(5, 32 * kConsWarps);
+    // M[l][j] (row-major 8 x 8): out = z M with z = [srcA - DA, srcB - DB]
+    if (threadIdx.x < 64) {
+      const int l = threadIdx.x >> 3, j = threadIdx.x & 7;
+      double v = 0.0;
+      if (l < 4 && j < 4) {
+        v = p.upd_a ? ep_ai[l + 4 * j] : 0.0;
+      } else if (l < 4) {  // -(TA^-1 W)[l][j-4]
+        if (p.upd_a && p.upd_b) {
+          double acc = 0.0;
+          for (int m = 0; m < 4; ++m) acc += ep_ai[l + 4 * m] * ep_w[m + 4 * (j - 4)];
+          v = -acc;
+        }
+      } else if (j >= 4) {
+        v = p.upd_b ? ep_bi[(l - 4) + 4 * (j - 4)] : 0.0;
+      }
+      ep_m[l * 8 + j] = v;
+    }
+    bar_named(5, 32 * kConsWarps);
     // Update A fragments: m-tile q, row index i is chunk row 4 f(i) + q with
     // f(i) = (i >> 1) + 4 (i & 1), so lane (i, kk) reads rows 4f..4f+3 of tile column
     // 4j + kk with two LDS.128 (line 8j + 2kk + (i & 1), 1024 j past k-step 0).  The two
@@ -310,8 +355,22 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       if (it >= nst) break;
       const int slot = it % S;
       unsigned long long t0 = prof ? clock64() : 0;
+#ifdef BGS_STEP_STAMPS
+      const unsigned long long t_pre = k12_gtime();
+#endif
       mbar_wait(&full[slot], (it / S) & 1);
       unsigned long long t1 = prof ? clock64() : 0;
+#ifdef BGS_STEP_STAMPS
+      if (j == 0 && g == 0 && gtid == 0 && p.kp / p.s < 512) {
+        const unsigned long long t_ready = k12_gtime();
+        unsigned long long* o = g_k12_log + (size_t)(p.kp / p.s) * 8;
+        const unsigned long long tv[4] = {t_entry, t_wait, t_pre, t_ready};
+        for (int i = 0; i < 4; ++i) {
+          atomicMin(&o[2 * i], tv[i]);
+          atomicMax(&o[2 * i + 1], tv[i]);
+        }
+      }
+#endif
       if (prof) ph[0] += t1 - t0;
       if (tl && j < kTl) { tl[j * 6 + 0] = t0; tl[j * 6 + 1] = t1; }
       const uint32_t base = sbase + (uint32_t)(slot * slot_bytes);
@@ -509,6 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         }
       }
     }
+    }  // live
   }
   if (pair) cluster_sync_all();  // no CTA leaves while its peer may still address its smem
 }
@@ -616,13 +676,22 @@ static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (p.cluster == 2) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (p.pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = p.cluster == 2 ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k, p);
 }
 

@@ -96,6 +96,7 @@ struct alignas(64) SplitParams {
   const DevStatus* status;
   unsigned long long* phase;
   int dbg;
+  int pdl;              // launched as a programmatic dependent of the merged reduce + step
 };
 // Plans the rank split for a fused Gram of the given shape; false when K12c does not
 // apply (then the caller uses tile_launch).  Fills own/ext ranges, slot_units, stages.

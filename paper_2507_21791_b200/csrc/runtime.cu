@@ -351,6 +351,15 @@ class Runner {
   bool prof_step = false;  // BGS_PROF_STEP: one profiler class per fused block step
   int gram_max_units = 0;  // BGS_GRAM_MAXUNITS (tests): chunk unfused Grams above this
   bool no_merge_small = false;  // BGS_NO_MERGE_SMALL: separate reduce and small launches
+  bool no_pdl = false;          // BGS_NO_PDL: no programmatic dependent launch of K12c
+  // Programmatic dependent launch of a fused kernel is allowed only right behind the
+  // merged reduce + step kernel (nothing queued in between): that kernel writes only the
+  // Gram, the small factors and the status word, which the fused kernel reads after its
+  // griddepcontrol.wait; X / Q come from kernels that completed before it started.
+  int merged_mark = -1, waits = 0, merged_waits = -1;
+  bool pdl_next() const {
+    return !no_pdl && merged_mark == c->launches && merged_waits == waits;
+  }
   int tile_dbg = 0;
   bool tile_prof = false;
 
@@ -367,6 +376,8 @@ class Runner {
     gram_max_units = e4 ? atoi(e4) : 0;
     const char* e5 = getenv("BGS_NO_MERGE_SMALL");
     no_merge_small = e5 && *e5 && *e5 != '0';
+    const char* e6 = getenv("BGS_NO_PDL");
+    no_pdl = e6 && *e6 && *e6 != '0';
     const char* d = getenv("BGS_TILE_DBG");
     tile_dbg = d ? atoi(d) : 0;
     const char* tp = getenv("BGS_TILE_PROF");
@@ -387,7 +398,7 @@ class Runner {
     if (!feed || col_end <= 0) return;
     const int upto = (int)std::min<long>((long)feed->ready.size(),
                                          (col_end + feed->chunk_cols - 1) / feed->chunk_cols);
-    for (; feed->waited < upto; ++feed->waited)
+    for (; feed->waited < upto; ++feed->waited, ++waits)
       CUDA_OK(cudaStreamWaitEvent(c->stream, feed->ready[feed->waited], 0));
   }
   void q_final(long col_end) {
@@ -575,6 +586,7 @@ class Runner {
         char cls[64] = "fused_update_gram";
         if (prof_step) snprintf(cls, sizeof cls, "fused_update_gram@kp%04d", fz.kp);
         Prof pr(c, cls, bytes, flops);
+        p.pdl = pdl_next() && !pr.a ? 1 : 0;  // (profiling events in between: plain launch)
         CUDA_OK(k12_launch(p, grid, c->stream, &c->launches));
         slot_base += grid / p.cluster;
       } else {
@@ -869,6 +881,8 @@ class Runner {
       Prof pr(c, "reduce_small", pend.bytes, 0.0);
       CUDA_OK(reduce_small_launch(pend.a, pend.entries, p, static_cast<unsigned*>(c->ticket.p),
                                   c->sms, c->stream, &c->launches));
+      merged_mark = c->launches;
+      merged_waits = waits;
       return;
     }
     flush_reduce();

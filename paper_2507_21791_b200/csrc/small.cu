@@ -408,7 +408,10 @@ BGS_DEV int trsm4_lanes(const double* g, const double* b, int s, double* w, int 
 }  // namespace
 
 #ifdef BGS_STEP_STAMPS
-__device__ unsigned long long g_st_min = ~0ull, g_st_red = 0ull, g_st[8];
+__device__ unsigned long long g_st_min = ~0ull, g_st_red = 0ull, g_st[8], g_st_log[512 * 8];
+extern "C" int bgs_dbg_step_stamps(unsigned long long* out) {  // 512 x 8, host memory
+  return (int)cudaMemcpyFromSymbol(out, g_st_log, sizeof g_st_log);
+}
 BGS_DEV unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -601,10 +604,11 @@ __device__ __forceinline__ void onesync_step4_body(const SmallParams& p) {
     }
 #ifdef BGS_STEP_STAMPS
     STAMP(6)
-    if (tid == 0 && kp % 40 == 0)
-      printf("[step stamps] kp %d: reduce %llu | last-detect %llu | pass %llu | products %llu | chol %llu | trsm %llu | chol2+stores %llu ns (entry->end %llu)\n",
-             kp, g_st_red - g_st_min, g_st[1] - g_st_red, g_st[2] - g_st[1], g_st[3] - g_st[2], g_st[4] - g_st[3],
-             g_st[5] - g_st[4], g_st[6] - g_st[5], g_st[6] - g_st_min);
+    if (tid == 0 && p.k < 512) {  // [k][start, reduce done, detect, pass, products, chol, trsm, end]
+      unsigned long long* o = g_st_log + (size_t)p.k * 8;
+      o[0] = g_st_min; o[1] = g_st_red;
+      for (int i = 1; i <= 6; ++i) o[i + 1] = g_st[i];
+    }
     if (tid == 0) {
       g_st_min = ~0ull;
       g_st_red = 0ull;
@@ -629,6 +633,10 @@ static_assert(RED_THREADS == kStepThreads, "one block shape for both halves");
 __global__ void __launch_bounds__(kStepThreads, 1)
     reduce_step4_kernel(const ReduceArgs r, int nblk, SmallParams p, unsigned* ticket) {
   __shared__ int last;
+  // The next fused kernel may launch now (programmatic dependent): its CTAs take the SMs
+  // this grid frees and prefetch their first stages; they wait for this grid to complete
+  // before reading anything it writes.
+  griddep_launch_dependents();
 #ifdef BGS_STEP_STAMPS
   const unsigned long long t_in = gtime();
 #endif
