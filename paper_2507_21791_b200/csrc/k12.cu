@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     // coefficients and hold finite data (the A block, or Q columns zeroed by the runtime).
     const int ksteps = (kcols + 3) / 4;
     const int jlast = max(ksteps - 1, 0);
+    const int kt_valid = kpart < ksteps ? (ksteps - 1 - kpart) / KS + 1 : 0;  // real k-steps
     double bco[KW];
 #pragma unroll
     for (int t = 0; t < KW; ++t) {
@@ -319,6 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     // folded in every kFold group-stages (<= 4 x 128 rows of plain fp64 per fold; folding
     // every stage costs ~7% of the kernel: the two_sums share the FP64 pipe with DMMA)
     constexpr int kFold = MTW >= 9 ? 1 : 4;  // (MTW = 9: registers for acc are short)
+    // Skipping padding DMMAs (warp-uniform branches) pays only in the widest instance
+    // (up to 3 of 9 tiles per warp are padding there: -12% at kp = 248..256); elsewhere the
+    // branches cost 2-4% of scheduling freedom (same-box A/B, tools/ab_perstep.sh).
+    constexpr bool kSkipPad = MTW >= 9;
     double hi[MTW][2], lo[MTW][2], acc[MTW][2];
 #pragma unroll
     for (int j = 0; j < MTW; ++j)
@@ -396,6 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         const uint32_t cb = base + (uint32_t)(qd * chunk_bytes);
 #pragma unroll
         for (int t = 0; t < KW; ++t) {
+          // (kSkipPad) padding k-steps (zero coefficients) at the end of a warp's range are
+          // skipped: warp-uniform, and adding their zero products would not change a bit
+          if (kSkipPad && t >= KW - 2 && t >= kt_valid) break;
           const int jk = min(kpart + KS * t, jlast);
           const uint32_t a = cb + 1024u * (uint32_t)jk;
           const double2 x0 = lds128(a + uoff0), x1 = lds128(a + uoff1);
@@ -517,10 +525,14 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
             double a0[4], a1[4];
             gfrag(acol[jp], a0);
             if (jp + 1 < MTW) gfrag(acol[jp + 1], a1);
+            // (kSkipPad) tiles past this rank's last output tile are dropped at the end: their
+            // DMMAs are skipped (warp-uniform; only the last two tiles of a warp can be such)
+            const bool v0 = !kSkipPad || jp < MTW - 2 || w + kGroupWarps * jp < mt_loc;
+            const bool v1 = !kSkipPad || jp + 1 < MTW - 2 || w + kGroupWarps * (jp + 1) < mt_loc;
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
-              dmma(acc[jp][0], acc[jp][1], a0[q4], b[q4]);
-              if (jp + 1 < MTW) dmma(acc[jp + 1][0], acc[jp + 1][1], a1[q4], b[q4]);
+              if (v0) dmma(acc[jp][0], acc[jp][1], a0[q4], b[q4]);
+              if (jp + 1 < MTW && v1) dmma(acc[jp + 1][0], acc[jp + 1][1], a1[q4], b[q4]);
             }
           }
         }
