@@ -594,6 +594,10 @@ namespace {
 // A-block unit and one span-1 unit -> mt <= KS KW / 2 + 2 (C = 1 and C = 2 alike)
 __host__ __device__ constexpr int mtw_for(int kw, int R) { return ((4 / R) * kw / 2 + 2 + 3) / 4; }
 constexpr int kKwMax = 16;
+// (KW, R) with a second instance at MTW = mtw_for(KW, R) - 1 (see k12_plan)
+__host__ __device__ constexpr bool has_narrow(int kw, int R) {
+  return (R == 1 && kw % 2 == 0) || (R == 2 && kw % 4 == 3);
+}
 
 struct Cand {
   int C, R;
@@ -663,9 +667,11 @@ bool k12_plan(SplitParams& p) {
     if (!S) continue;
     q.kw = kw_t;
     q.mtw = mtw_for(kw_t, cd.R);
-    // one narrower instance: KW = 16 at R = 1 would carry MTW = 9 (folds every stage,
-    // spills) where 8 tiles per warp suffice (kp = 244..252 at s = 4)
-    if (cd.R == 1 && kw_t == 16 && mtw <= 8) q.mtw = 8;
+    // narrower instances (has_narrow): mtw_for(KW) carries one output tile per warp more
+    // than the split needs at 1-5 steps of these KW (CTA pairs at s = 4: kp = 292..308 need
+    // MTW 5 at KW 10, kp = 356..372 MTW 6 at KW 12, -5% each; one CTA: KW 16 would fold
+    // every stage and spill at MTW 9 where 8 suffice)
+    if (has_narrow(kw_t, cd.R) && mtw <= mtw_for(kw_t, cd.R) - 1) q.mtw = mtw_for(kw_t, cd.R) - 1;
     q.stages = S;
     p = q;
     static const bool verbose = getenv("BGS_K12C_VERBOSE") != nullptr;
@@ -709,7 +715,19 @@ static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
 
 template <int R>
 static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
-  if (R == 1 && p.kw == 16 && p.mtw == 8) return launch_k12<16, 1, 8>(p, grid, st);
+  if (p.mtw == mtw_for(p.kw, R) - 1) {
+    switch (p.kw) {
+#define BGS_NKW(K) \
+  case K:          \
+    if constexpr (has_narrow(K, R)) return launch_k12<K, R, mtw_for(K, R) - 1>(p, grid, st); \
+    break;
+      BGS_NKW(2) BGS_NKW(3) BGS_NKW(4) BGS_NKW(6) BGS_NKW(7) BGS_NKW(8) BGS_NKW(10)
+      BGS_NKW(11) BGS_NKW(12) BGS_NKW(14) BGS_NKW(15) BGS_NKW(16)
+#undef BGS_NKW
+      default: break;
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (p.kw) {
 #define BGS_KW(K) \
   case K: return launch_k12<K, R>(p, grid, st);
