@@ -317,9 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     }
 
     // (hi, lo) double-double per output; the stage contractions accumulate in acc and are
-    // folded in every kFold group-stages (<= 4 x 128 rows of plain fp64 per fold; folding
-    // every stage costs ~7% of the kernel: the two_sums share the FP64 pipe with DMMA)
-    constexpr int kFold = MTW >= 9 ? 1 : 4;  // (MTW = 9: registers for acc are short)
+    // folded in every kFold = 16 / R group-stages (<= 512 rows of plain fp64 per fold at
+    // every R; folding every stage costs ~7% of the kernel: the two_sums share the FP64
+    // pipe with DMMA; 4 stages at R = 1 cost 0.3 ms more than 16 at config 2)
+    constexpr int kFold = MTW >= 9 ? 1 : 16 / R;  // (MTW = 9: registers for acc are short)
     // Skipping padding DMMAs (warp-uniform branches) pays only in the widest instance
     // (up to 3 of 9 tiles per warp are padding there: -12% at kp = 248..256); elsewhere the
     // branches cost 2-4% of scheduling freedom (same-box A/B, tools/ab_perstep.sh).
