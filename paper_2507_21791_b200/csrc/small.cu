@@ -59,38 +59,56 @@ __device__ __noinline__ void cta_atb(const double* A, int lda, const double* B, 
   }
 }
 
-// Upper Cholesky of the symmetrized a (s x s) into g; returns the 1-based failing pivot.
-// Thread-serial: s <= 16 (chol_factor, dense_kernels.cpp:54-87).
-__device__ __noinline__ int chol_serial(const double* a, int s, double* g) {
-  for (int k = 0; k < s * s; ++k) g[k] = 0.0;
-  for (int j = 0; j < s; ++j) {
-    for (int i = 0; i <= j; ++i) {
+// Upper Cholesky of the symmetrized a (s x s) into g (shared); returns the 1-based failing
+// pivot on every lane (chol_factor, dense_kernels.cpp:54-87).  One warp, lane j owning
+// column j (s <= 16): rows are finished in order -- the diagonal on lane i, then row i's
+// divisions in parallel.  Entry (i, j) = (0.5 (a_ij + a_ji) - sum_{k<i} g_ki g_kj) / g_ii
+// with the same k order as the serial loop, so the result is the same bit for bit and the
+// first failing pivot is the same; the chain is s square roots + s divisions instead of
+// s (s + 1) / 2 dependent fp64 divisions / roots on one thread.
+__device__ __noinline__ int chol_warp(const double* a, int s, double* g) {
+  const int lane = threadIdx.x & 31;
+  for (int k = lane; k < s * s; k += 32) g[k] = 0.0;
+  __syncwarp();
+  for (int i = 0; i < s; ++i) {
+    double d = 0.0;
+    if (lane == i) {
+      double acc = 0.5 * (a[i + i * s] + a[i + i * s]);
+      for (int k = 0; k < i; ++k) acc -= g[k + i * s] * g[k + i * s];
+      d = acc;
+    }
+    d = __shfl_sync(0xffffffffu, d, i);
+    if (!(d > 0.0)) return i + 1;
+    const double gii = sqrt(d);
+    if (lane > i && lane < s) {
+      const int j = lane;
       double acc = 0.5 * (a[i + j * s] + a[j + i * s]);
       for (int k = 0; k < i; ++k) acc -= g[k + i * s] * g[k + j * s];
-      if (i == j) {
-        if (!(acc > 0.0)) return j + 1;
-        g[j + j * s] = sqrt(acc);
-      } else {
-        g[i + j * s] = acc / g[i + i * s];
-      }
+      g[i + j * s] = acc / gii;
     }
+    if (lane == i) g[i + i * s] = gii;
+    __syncwarp();
   }
   return 0;
 }
 
-// W = G^{-T} B for upper G (s x s), B (s x s) (tri_solve_left_trans).  Returns 1-based
-// index of a zero diagonal entry (SingularError), else 0.
-__device__ __noinline__ int trsm_lt_serial(const double* g, int ldg_, const double* b, int ldb, int s,
-                              double* w) {
-  for (int i = 0; i < s; ++i) {
-    const double gii = g[i + i * ldg_];
-    if (gii == 0.0) return i + 1;
-    for (int j = 0; j < s; ++j) {
+// W = G^{-T} B for upper G (s x s), B (s x s) (tri_solve_left_trans), one warp: lane j
+// solves column j (same expressions and order as the row-serial loop).  Returns the
+// 1-based index of the first zero diagonal entry (SingularError) on every lane, else 0.
+__device__ __noinline__ int trsm_lt_warp(const double* g, int ldg_, const double* b, int ldb, int s,
+                                         double* w) {
+  const int lane = threadIdx.x & 31;
+  for (int i = 0; i < s; ++i)
+    if (g[i + i * ldg_] == 0.0) return i + 1;
+  if (lane < s) {
+    const int j = lane;
+    for (int i = 0; i < s; ++i) {
       double acc = b[i + j * ldb];
       for (int k = 0; k < i; ++k) acc -= g[k + i * ldg_] * w[k + j * s];
-      w[i + j * s] = acc / gii;
+      w[i + j * s] = acc / g[i + i * ldg_];
     }
   }
+  __syncwarp();
   return 0;
 }
 
@@ -193,9 +211,12 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
         const int i = e % s, j = e / s;
         p.R[i + (size_t)j * p.ldr] = i <= j ? sh.b[e] : 0.0;
       }
-      if (tid == 0) {
-        sh.pivot = trsm_lt_serial(sh.b, s, p.G, p.ldg, s, sh.a);
-        if (sh.pivot) set_status(p.status, ST_SINGULAR, sh.pivot, 1, SITE_NONE, 0);
+      if (tid < 32) {
+        const int piv = trsm_lt_warp(sh.b, s, p.G, p.ldg, s, sh.a);
+        if (tid == 0) {
+          sh.pivot = piv;
+          if (piv) set_status(p.status, ST_SINGULAR, piv, 1, SITE_NONE, 0);
+        }
       }
       __syncthreads();
       if (sh.pivot) return;
@@ -205,12 +226,14 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
         // S_diag = chol(T2 - scol^T scol)  (bcgs.cpp:280-287)
         cta_atb(sh.a, s, sh.a, s, s, s, sh.c);
         __syncthreads();
-        if (tid == 0) {
-          for (int e = 0; e < s * s; ++e)
+        if (tid < 32) {
+          for (int e = tid; e < s * s; e += 32)
             sh.c[e] = p.G[(s + e % s) + (size_t)(e / s) * p.ldg] - sh.c[e];
-          const int piv = chol_serial(sh.c, s, sh.d);
-          if (piv) set_status(p.status, ST_NOT_SPD, piv, 2, SITE_PROLOGUE_PYTH, p.kappa_power);
-          for (int e = 0; e < s * s; ++e) p.sdiag[e] = sh.d[e];
+          __syncwarp();
+          const int piv = chol_warp(sh.c, s, sh.d);
+          if (piv && tid == 0) set_status(p.status, ST_NOT_SPD, piv, 2, SITE_PROLOGUE_PYTH, p.kappa_power);
+          __syncwarp();
+          for (int e = tid; e < s * s; e += 32) p.sdiag[e] = sh.d[e];
         }
       } else if (p.os_mode == OS_SKIP) {
         for (int e = tid; e < s * s; e += kThreads) p.sdiag[e] = (e % s == e / s) ? 1.0 : 0.0;
@@ -223,11 +246,14 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       // Y^T Y, then Y_diag = chol(Omega - Y^T Y)  (bcgs.cpp:321-327)
       cta_atb(Y, p.ldg, Y, p.ldg, kp, s, sh.a);
       __syncthreads();
-      if (tid == 0) {
-        for (int e = 0; e < s * s; ++e) sh.c[e] = Om[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
-        sh.pivot = chol_serial(sh.c, s, sh.d);
-        if (sh.pivot)
-          set_status(p.status, ST_NOT_SPD, sh.pivot, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
+      if (tid < 32) {
+        for (int e = tid; e < s * s; e += 32) sh.c[e] = Om[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
+        __syncwarp();
+        const int piv = chol_warp(sh.c, s, sh.d);
+        if (tid == 0) {
+          sh.pivot = piv;
+          if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
+        }
       }
       __syncthreads();
       if (sh.pivot) return;
@@ -241,10 +267,14 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       const double* P = p.G + kp + (size_t)s * p.ldg;
       cta_atb(Y, p.ldg, Z, p.ldg, kp, s, sh.a);
       __syncthreads();
-      if (tid == 0) {
-        for (int e = 0; e < s * s; ++e) sh.b[e] = P[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
-        sh.pivot = trsm_lt_serial(sh.d, s, sh.b, s, s, sh.c);
-        if (sh.pivot) set_status(p.status, ST_SINGULAR, sh.pivot, p.k + 1, SITE_NONE, 0);
+      if (tid < 32) {
+        for (int e = tid; e < s * s; e += 32) sh.b[e] = P[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
+        __syncwarp();
+        const int piv = trsm_lt_warp(sh.d, s, sh.b, s, s, sh.c);
+        if (tid == 0) {
+          sh.pivot = piv;
+          if (piv) set_status(p.status, ST_SINGULAR, piv, p.k + 1, SITE_NONE, 0);
+        }
       }
       __syncthreads();
       if (sh.pivot) return;
@@ -260,12 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
         // S_diag = chol(T - scol^T scol)  (bcgs.cpp:352-359)
         cta_atb(snext, kn, snext, kn, kn, s, sh.a);
         __syncthreads();
-        if (tid == 0) {
+        if (tid < 32) {
           const double* T = p.G + kp + s + (size_t)s * p.ldg;
-          for (int e = 0; e < s * s; ++e) sh.b[e] = T[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
-          const int piv = chol_serial(sh.b, s, sh.c);
-          if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 2, SITE_FIRST_PASS, p.kappa_power);
-          for (int e = 0; e < s * s; ++e) p.sdiag[e] = sh.c[e];
+          for (int e = tid; e < s * s; e += 32) sh.b[e] = T[(e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
+          __syncwarp();
+          const int piv = chol_warp(sh.b, s, sh.c);
+          if (piv && tid == 0) set_status(p.status, ST_NOT_SPD, piv, p.k + 2, SITE_FIRST_PASS, p.kappa_power);
+          __syncwarp();
+          for (int e = tid; e < s * s; e += 32) p.sdiag[e] = sh.c[e];
         }
       } else if (p.os_mode == OS_SKIP) {
         for (int e = tid; e < s * s; e += kThreads) p.sdiag[e] = (e % s == e / s) ? 1.0 : 0.0;
@@ -278,11 +310,13 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
         p.save[(e % kp) + (size_t)(e / kp) * p.ldsave] = p.G[(e % kp) + (size_t)(e / kp) * p.ldg];
       cta_atb(p.G, p.ldg, p.G, p.ldg, kp, s, sh.a);
       __syncthreads();
-      if (tid == 0) {
-        for (int e = 0; e < s * s; ++e) sh.b[e] = p.G[(kp + e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
-        const int piv = chol_serial(sh.b, s, sh.d);
-        if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_FIRST_PASS, p.kappa_power);
-        for (int e = 0; e < s * s; ++e) p.sdiag[e] = sh.d[e];
+      if (tid < 32) {
+        for (int e = tid; e < s * s; e += 32) sh.b[e] = p.G[(kp + e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
+        __syncwarp();
+        const int piv = chol_warp(sh.b, s, sh.d);
+        if (piv && tid == 0) set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_FIRST_PASS, p.kappa_power);
+        __syncwarp();
+        for (int e = tid; e < s * s; e += 32) p.sdiag[e] = sh.d[e];
       }
       return;
     }
@@ -290,11 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       // [Y; Omega] = [Q U]^T U -> Y_diag = chol(Omega - Y^T Y); R column  (bcgs.cpp:199-216)
       cta_atb(p.G, p.ldg, p.G, p.ldg, kp, s, sh.a);
       __syncthreads();
-      if (tid == 0) {
-        for (int e = 0; e < s * s; ++e) sh.b[e] = p.G[(kp + e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
-        sh.pivot = chol_serial(sh.b, s, sh.d);
-        if (sh.pivot)
-          set_status(p.status, ST_NOT_SPD, sh.pivot, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
+      if (tid < 32) {
+        for (int e = tid; e < s * s; e += 32) sh.b[e] = p.G[(kp + e % s) + (size_t)(e / s) * p.ldg] - sh.a[e];
+        __syncwarp();
+        const int piv = chol_warp(sh.b, s, sh.d);
+        if (tid == 0) {
+          sh.pivot = piv;
+          if (piv) set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_SECOND_PASS, p.kappa_power);
+        }
       }
       __syncthreads();
       if (sh.pivot) return;
@@ -330,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
 //  3. the s x s factors on lanes 0..3 of warp 0, lane j owning column j: Cholesky row by
 //     row (the diagonal on lane i, then the divisions of row i in parallel), triangular
 //     solves column-parallel.
-// Every entry is formed by the same expression as chol_serial / trsm_lt_serial / r_diag
+// Every entry is formed by the same expression as chol_warp / trsm_lt_warp / r_diag
 // (symmetrization, the k-ordered updates, the !(acc > 0) pivot test, division by the
 // diagonal); only the kp-long sums are grouped differently (the reference forms them
 // sequentially, this path by row chunks).
@@ -360,7 +397,7 @@ BGS_DEV void product_cols(int e, int& cu, int& cv) {
 // Upper Cholesky of the symmetrized s x s block a (column-major 4 x 4) into g (shared),
 // on lanes 0..3 of one warp; every lane returns the same 1-based failing pivot (0 = ok).
 // Entry (i, j) = (0.5 (a_ij + a_ji) - sum_{k<i} g_ki g_kj) / g_ii, diagonal by sqrt --
-// the chol_serial expression; rows are finished in order, so the first failing pivot is
+// the chol_warp expression; rows are finished in order, so the first failing pivot is
 // the same as in the column-ordered loop.
 BGS_DEV int chol4_lanes(const double* a, int s, double* g, int lane) {
   if (lane < 16) g[lane] = 0.0;
