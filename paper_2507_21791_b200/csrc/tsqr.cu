@@ -220,7 +220,7 @@ __device__ __forceinline__ void cta_sum_t(double (&v)[NV], double* scratch /*[8]
 }
 
 template <int S, int RPT>
-__global__ void __launch_bounds__(kLeafThreads, S <= 4 ? 3 : 1)  // 3 leaves per SM for s <= 4
+__global__ void __launch_bounds__(kLeafThreads, S <= 8 ? 3 : 2)  // 3 leaves per SM for s <= 8, else 2
     tsqr_leaf_reg_kernel(const double* __restrict__ src, long lds, double* __restrict__ dst,
                          long ldd, const long* __restrict__ leaf_row0,
                          double* __restrict__ rleaf, const DevStatus* status) {
@@ -667,7 +667,8 @@ struct TreeGroupArgs {
 };
 
 template <int S>  // S = 0: runtime s (generic pair QR)
-__global__ void __launch_bounds__(512) tsqr_up_group_kernel(const TreeGroupArgs a,
+// (S = 16: 256 threads so a warp's pair QR gets the registers it needs; 512 spilled)
+__global__ void __launch_bounds__(S >= 16 ? 256 : 512) tsqr_up_group_kernel(const TreeGroupArgs a,
                                                             const DevStatus* status) {
   if (status && status_bad(status)) return;
   extern __shared__ double tsm[];
@@ -786,7 +787,7 @@ cudaError_t tsqr_tree_up_shard(double* ws, int L, int leaf_base, int Lt, int s, 
     a.out = j + 1 == t.launches.size() ? root_out : bufs[(j + 1) & 1];
     const int groups = (t.cnt[l0] + (1 << D) - 1) >> D;
     const size_t smem = (size_t)2 * (1 << D) * ss * sizeof(double);
-    const int threads = 32 * std::max(1, (1 << D) / 2);
+    const int threads = std::min(s >= 16 ? 256 : 512, 32 * std::max(1, (1 << D) / 2));
     cudaError_t e = cudaSuccess;
 #define BGS_UP_GROUP(S_)                                                        \
   {                                                                           \
@@ -867,7 +868,7 @@ __global__ void __launch_bounds__(256)
   if (status && status_bad(status)) return;
   constexpr int SS = S * S;
   __shared__ double hq[S <= 8 ? 32 : 20][SS];  // (static shared memory <= 48 KB)
-  __shared__ double mm[2][SS];
+  __shared__ __align__(16) double mm[2][SS];
   const int l = blockIdx.x, tid = threadIdx.x;
   const int nh = tp.nlev - 1;  // levels with nodes below the root
   // every path factor at once (independent L2 reads); pass-throughs become identities
@@ -908,20 +909,42 @@ __global__ void __launch_bounds__(256)
   if (tid == 0) cur_s = cur;
   __syncthreads();
   const double* m = mm[cur_s];
-  double mr[SS];
-#pragma unroll
-  for (int e = 0; e < SS; ++e) mr[e] = m[e];
   const long g0 = leaf_row0[l], g1 = leaf_row0[l + 1];
-  for (long i = g0 + tid; i < g1; i += blockDim.x) {
-    double row[S];
+  if constexpr (S <= 8) {
+    double mr[SS];
 #pragma unroll
-    for (int j = 0; j < S; ++j) row[j] = dst[i + (size_t)j * ldd];
+    for (int e = 0; e < SS; ++e) mr[e] = m[e];
+    for (long i = g0 + tid; i < g1; i += blockDim.x) {
+      double row[S];
 #pragma unroll
-    for (int j = 0; j < S; ++j) {
-      double acc = 0.0;
+      for (int j = 0; j < S; ++j) row[j] = dst[i + (size_t)j * ldd];
 #pragma unroll
-      for (int k = 0; k < S; ++k) acc = fma(row[k], mr[k + j * S], acc);
-      dst[i + (size_t)j * ldd] = acc;
+      for (int j = 0; j < S; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < S; ++k) acc = fma(row[k], mr[k + j * S], acc);
+        dst[i + (size_t)j * ldd] = acc;
+      }
+    }
+  } else {
+    // S = 16: M (2 KB) stays in shared memory (broadcast reads, two entries per load); in
+    // registers it spilled 1.8 KB per thread.  Same products in the same order.
+    for (long i = g0 + tid; i < g1; i += blockDim.x) {
+      double row[S];
+#pragma unroll
+      for (int j = 0; j < S; ++j) row[j] = dst[i + (size_t)j * ldd];
+#pragma unroll 4
+      for (int j = 0; j < S; ++j) {
+        const double2* mc = reinterpret_cast<const double2*>(m + j * S);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < S; k += 2) {
+          const double2 t = mc[k / 2];
+          acc = fma(row[k], t.x, acc);
+          acc = fma(row[k + 1], t.y, acc);
+        }
+        dst[i + (size_t)j * ldd] = acc;
+      }
     }
   }
 }
