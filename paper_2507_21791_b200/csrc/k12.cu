@@ -370,11 +370,12 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       if (j == 0 && g == 0 && gtid == 0 && p.kp / p.s < 512) {
         const unsigned long long t_ready = k12_gtime();
         unsigned long long* o = g_k12_log + (size_t)(p.kp / p.s) * 8;
-        const unsigned long long tv[4] = {t_entry, t_wait, t_pre, t_ready};
-        for (int i = 0; i < 4; ++i) {
-          atomicMin(&o[2 * i], tv[i]);
-          atomicMax(&o[2 * i + 1], tv[i]);
-        }
+        // [min, max] of: entry (0, 1), dependency wait released (2, 3), first stage ready
+        // (6, 7); the CTA end goes to (4, 5) at the bottom of the kernel
+        (void)t_pre;
+        atomicMin(&o[0], t_entry); atomicMax(&o[1], t_entry);
+        atomicMin(&o[2], t_wait);  atomicMax(&o[3], t_wait);
+        atomicMin(&o[6], t_ready); atomicMax(&o[7], t_ready);
       }
 #endif
       if (prof) ph[0] += t1 - t0;
@@ -584,6 +585,13 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     }  // live
   }
   if (pair) cluster_sync_all();  // no CTA leaves while its peer may still address its smem
+#ifdef BGS_STEP_STAMPS
+  if (threadIdx.x == 0 && p.kp / p.s < 512) {
+    const unsigned long long t_end = k12_gtime();
+    atomicMin(&g_k12_log[(size_t)(p.kp / p.s) * 8 + 4], t_end);
+    atomicMax(&g_k12_log[(size_t)(p.kp / p.s) * 8 + 5], t_end);
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------------------

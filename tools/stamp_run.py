@@ -21,17 +21,15 @@ lib.bgs_dbg_step_stamps(ctypes.c_void_p(st.ctypes.data))
 lib.bgs_dbg_k12_stamps(ctypes.c_void_p(kt.ctypes.data), 0)
 st = st.reshape(512, 8).astype(np.int64); kt = kt.reshape(512, 8).astype(np.int64)
 print("factor ms", tm.factor_ms)
-gaps, rdy, dur = [], [], []
+gaps, rdy, dur, spread, kdur = [], [], [], [], []
 for k in range(1, m // s - 1):
     end = st[k, 7]
-    e0, e1, w0, w1, f0, f1, r0, r1 = kt[k] - end
-    gaps.append(e0); rdy.append(r1); dur.append(st[k, 7] - st[k, 0])
+    e0, e1, w0, w1, x0, x1, r0, r1 = kt[k]
+    gaps.append(e0 - end); rdy.append(r1 - end); dur.append(st[k, 7] - st[k, 0])
+    spread.append(x1 - x0); kdur.append(x1 - e0)
     if k % 10 == 0:
-        print(f"k {k:3d} step {st[k,7]-st[k,0]:6d} ns | relative to step end: entry {e0:6d}..{e1:6d} "
-              f"wait released {w0:6d}..{w1:6d} setup done {f0:6d}..{f1:6d} ready {r0:6d}..{r1:6d}")
-print("mean step", np.mean(dur), "mean first entry", np.mean(gaps), "mean last ready", np.mean(rdy))
-if len(sys.argv) > 1:  # per step: consumer setup time (wait release -> first stage wait), max over CTAs
-    print("k setup_ns(min..max)")
-    for k in range(1, m // s - 1):
-        e0, e1, w0, w1, f0, f1, r0, r1 = kt[k]
-        print(k, f0 - w1, f1 - w0)
+        print(f"k {k:3d} step {st[k,7]-st[k,0]:6d} ns | vs step end: entry {e0-end:6d}..{e1-end:6d} "
+              f"wait released {w0-end:6d}..{w1-end:6d} ready {r0-end:6d}..{r1-end:6d} | "
+              f"CTA ends spread {x1-x0:6d} of kernel {x1-e0:7d}")
+print("mean step", np.mean(dur), "mean first entry", np.mean(gaps), "mean last ready", np.mean(rdy),
+      "mean CTA-end spread", np.mean(spread), "sum spread ms", np.sum(spread) / 1e6)
