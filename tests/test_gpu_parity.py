@@ -181,6 +181,38 @@ def test_not_spd_diagnostic(oracle, gpu_ctx, v):
         assert ref.rc != 0 or oracle.loo(out.q) > 1e-8
 
 
+@pytest.mark.parametrize("kappa", [1e2, 1e4, 1e6, 1e10, 1e12])
+@pytest.mark.parametrize("v", VARIANTS, ids=lambda v: NAMES[v])
+def test_stability_ladder(oracle, gpu_ctx, v, kappa):
+    """acceptance.cpp:227-366's ladder on geometric X (n = 1000, m = 32, s = 4).  Inside the
+    working assumption (u kappa^2 << 1) every variant succeeds with LOO / residual within
+    10x of the reference's.  Far outside it the two-sync reorthogonalized variants
+    (BCGSI+, BCGSI+P-2S) and BCGSI+1S still succeed at the u level, as in the reference;
+    the Pythagorean one-pass variants (BCGSI+P-1S, BCGSPIPI+) abort NotSpd wherever the
+    reference does, and may abort earlier than the reference: its exactly rounded Gram
+    keeps T - S^T S positive a little longer (kappa = 1e10 here) than fp64 tensor-core
+    sums with double-double folds do."""
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 1000, 32, 4
+    x = oracle.gen_matrix(n, m, s, kappa, 12345, False)
+    ref = oracle.factor(v, x, s, 1, metrics=True)
+    out = bgs.run_factor(v, x, s, 1, metrics=False)
+    pythagorean = NAMES[v] in ("BCGSI+P-1S", "BCGSPIPI+")
+    if U * kappa * kappa < 1e-3 or not pythagorean:
+        assert (ref.rc == 0) == out.ok, (out.error, ref.msg)
+    if ref.rc != 0:
+        assert not out.ok
+    if out.ok:
+        assert ref.rc == 0
+        assert_structure(out.r)
+        loo, res = oracle.loo(out.q), oracle.residual(x, out.q, out.r)
+        assert loo <= 10 * max(ref.loo, U), (loo, ref.loo)
+        assert res <= 10 * max(ref.resid, U), (res, ref.resid)
+    else:
+        assert out.not_spd_pivot >= 1 and NAMES[v] in out.error
+        assert "likely violated working assumption" in out.error
+
+
 def test_not_spd_matches_oracle_message_when_both_abort(oracle, gpu_ctx):
     """Far outside u*kappa^2 <= 1 both paths abort; WHERE the first non-positive pivot
     appears depends on rounding (the reference's Gram is exact, ours is fp64), so the
