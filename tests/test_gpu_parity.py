@@ -331,17 +331,23 @@ def test_procs_change_only_rounding(oracle, gpu_ctx):
 
 @pytest.mark.parametrize("v,procs", [(3, 1), (3, 3), (2, 1), (4, 2), (1, 1)],
                          ids=lambda p: str(p))
-def test_streamed_host_io_is_bitwise_identical(gpu_ctx, v, procs):
-    """bgs_factor with pinned host buffers streams X in / Q out on copy engines while the
-    sweep runs; the result must be bit-identical to the staged copy path."""
+def test_streamed_host_io_is_bitwise_identical(gpu_ctx, monkeypatch, v, procs):
+    """bgs_factor streams X in / Q out on copy engines while the sweep runs -- straight from
+    pinned host buffers, through rings of pinned slots (feeder / drainer threads) from
+    pageable ones; both must be bit-identical to the staged copy path."""
     import ctypes
     import torch
     from paper_2507_21791_b200 import api
     import paper_2507_21791_b200 as bgs
     n, m, s = 70001, 96, 4
     x = bgs.gen_gaussian_host(777, n, m)
+    monkeypatch.setenv("BGS_NO_STREAM_IO", "1")
     staged = bgs.run_factor(v, x, s, procs, metrics=False, ctx=gpu_ctx)
+    monkeypatch.delenv("BGS_NO_STREAM_IO")
     assert staged.ok
+    pageable = bgs.run_factor(v, x, s, procs, metrics=False, ctx=gpu_ctx)
+    assert pageable.ok
+    assert np.array_equal(pageable.q, staged.q) and np.array_equal(pageable.r, staged.r)
     hx = torch.from_numpy(np.asfortranarray(x).T.copy()).pin_memory()  # (m, n) = column-major n x m
     hq = torch.zeros((m, n), dtype=torch.float64).pin_memory()
     r = np.zeros((m, m), order="F")
