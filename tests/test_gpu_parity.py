@@ -284,6 +284,38 @@ def test_square_and_minimal_shapes(oracle, gpu_ctx, v, n, m, s):
     assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
 
 
+@pytest.mark.parametrize("shape", [(0, 0, 1), (5, 0, 1), (0, 4, 4), (3, 4, 4)])
+def test_empty_and_short_inputs_rejected_like_reference(oracle, gpu_ctx, shape):
+    """Empty X and n < m: DimensionError with the reference's wording (bcgs.cpp:14-26)."""
+    import paper_2507_21791_b200 as bgs
+    from oracle.oracle import Reference
+    n, m, s = shape
+    x = np.zeros((n, m), order="F")
+    ref = Reference().factor(3, x, s, 1, metrics=False)
+    assert ref.rc != 0
+    with pytest.raises(bgs.api.DimensionError) as e:
+        bgs.run_factor(3, x, s, 1, metrics=False)
+    assert str(e.value).split(": ", 1)[-1].startswith(ref.msg.split(": ", 1)[-1][:30])
+
+
+@pytest.mark.parametrize("v", VARIANTS, ids=lambda v: NAMES[v])
+@pytest.mark.parametrize("n,m,s,procs", [(8, 4, 4, 16), (10, 8, 2, 7), (33, 32, 16, 5)])
+def test_more_ranks_than_rows(oracle, gpu_ctx, v, n, m, s, procs):
+    """procs with empty or one-row shards (the ceil split leaves trailing ranks empty):
+    same sync accounting as the reference, R to 1e-10, LOO within 10x."""
+    import paper_2507_21791_b200 as bgs
+    x = oracle.gen_matrix(n, m, s, 10.0, 4242, False)
+    ref = oracle.factor(v, x, s, procs, metrics=True)
+    assert ref.rc == 0
+    out = bgs.run_factor(v, x, s, procs, metrics=False)
+    assert out.ok, out.error
+    assert out.stats.sync_count == ref.sync_count
+    assert out.stats.event_labels == ref.labels
+    assert_structure(out.r)
+    assert_r_close(out.r, ref.r)
+    assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
+
+
 def test_malformed_inputs_rejected(gpu_ctx):
     import paper_2507_21791_b200 as bgs
     x = np.random.default_rng(2).standard_normal((16, 6))
