@@ -605,3 +605,37 @@ def test_nccl_path_on_one_rank_matches_local_path(oracle, gpu_ctx, v):
     assert np.array_equal(r0, r1) and np.array_equal(q0, q1)
     ref = oracle.factor(v, x, s, 1, metrics=False)
     assert_r_close(r1, ref.r)
+
+
+def test_sweep_driver_end_to_end(tmp_path):
+    """The report driver (bench.cpp:253-394 schema) runs every variant on the GPU: one row
+    per (cell, variant), exact counters, u-level LOO for the i.i.d. cell, the measured
+    speedup against BCGSI+ at s = 1 filled in, and the expected-failure column set from
+    the variant's working assumption at kappa = 1e12."""
+    import csv
+    import subprocess
+    import sys
+    import paper_2507_21791_b200 as bgs
+    out = tmp_path / "sweep.csv"
+    r = subprocess.run([sys.executable, "-m", "paper_2507_21791_b200.sweep", "--variants", "all",
+                        "--n", "20000", "--m", "32", "--s", "4", "--kappa", "1,1e12",
+                        "--repeats", "1", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = list(csv.DictReader(open(out)))
+    assert len(rows) == 2 * 5
+    for row in rows:
+        v = int(bgs.parse_variant(row["variant"]))
+        failed = row["loo"].lower() == "nan"
+        # failed cells carry zero counters, like the reference (bench.cpp:344-347)
+        assert int(row["sync_count"]) == (0 if failed else bgs.expected_syncs(v, 8))
+        if float(row["kappa"]) == 1.0:
+            assert not failed
+            assert float(row["loo"]) < 1e-14 and float(row["predicted_time"]) > 0
+            assert float(row["speedup_vs_bcgsi+"]) > 0
+    # at kappa = 1e12 only variants whose working assumption u kappa^p <= 1 is violated
+    # may abort (p = 2 for the Pythagorean ones, 3 for BCGSI+1S; variant.cpp:88-104)
+    for row in rows:
+        if row["loo"].lower() == "nan":
+            assert float(row["kappa"]) > 1
+            assert row["variant"] in ("BCGSI+P-1S", "BCGSPIPI+", "BCGSI+1S"), row["variant"]
