@@ -253,9 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant
     const long row0 = (st0 + it) * RS;
     const int vrows = (int)((p.n_rows - row0) < RS ? (p.n_rows - row0) : RS);
     if (vrows < RS) {
-      // rows past the shard end inside the last 16-row block are not TMA zero-filled
+      // rows past the shard end inside the last 16-row block are not TMA zero-filled;
+      // (only the WG warps of the stage loop run this: K1's producer warp has left)
       const int ncol = p.units * 8;
-      for (int e = threadIdx.x; e < ncol * (RS - vrows); e += 32 * W) {
+      for (int e = threadIdx.x; e < ncol * (RS - vrows); e += 32 * WG) {
         const int c = e / (RS - vrows), r = vrows + e % (RS - vrows);
         sts64(base + elem_off<H>(c, r), 0.0);
       }

@@ -184,6 +184,8 @@ struct DBuf {
     bytes = 0;
     CUDA_OK(cudaMalloc(&p, b));
     bytes = b;
+    static const bool poison = getenv("BGS_POISON") != nullptr;  // tests: NaN-fill new buffers
+    if (poison) CUDA_OK(cudaMemset(p, 0xFF, b));
   }
   void release() {
     if (p) cudaFree(p);
@@ -1384,6 +1386,7 @@ class Runner {
       f.msg = buf;
     } else if (h.code == ST_NON_FINITE) {
       f.msg = "reduction saw a NaN or infinity";
+      if (getenv("BGS_DEBUG_STATUS")) f.msg += " (block column " + std::to_string(h.block) + ")";
     } else if (h.code == ST_SINGULAR) {
       f.msg = "triangular factor has a zero at diagonal entry " + std::to_string(h.pivot);
     } else {

@@ -639,3 +639,43 @@ def test_sweep_driver_end_to_end(tmp_path):
         if row["loo"].lower() == "nan":
             assert float(row["kappa"]) > 1
             assert row["variant"] in ("BCGSI+P-1S", "BCGSPIPI+", "BCGSI+1S"), row["variant"]
+
+
+def test_no_reads_of_uninitialized_device_memory():
+    """Every device buffer the library allocates is NaN-filled on allocation
+    (BGS_POISON=1, a fresh process): any read of memory that was never written -- padding
+    rows of a stage, unwritten Gram slots, stale workspace -- turns into NaN and fails the
+    factorization.  Ragged shard sizes, tiny shards, every variant, s = 1..16."""
+    import os
+    import subprocess
+    import sys
+    script = r'''
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2507_21791_b200 as bgs
+from oracle.oracle import Oracle
+o = Oracle()
+bad = []
+for (n, m, s, P) in [(33, 32, 16, 5), (100, 8, 4, 1), (1000, 32, 4, 3), (2000, 48, 8, 2),
+                     (5000, 40, 4, 1), (3001, 64, 16, 1), (10, 8, 2, 7), (777, 24, 3, 2)]:
+    x = o.gen_matrix(n, m, s, 10.0, 4242, False)
+    ctx = bgs.Context(0)  # fresh (NaN-filled) buffers for every shape
+    for v in [1, 2, 3, 4, 5]:
+        ref = o.factor(v, x, s, P, metrics=False)
+        try:
+            out = bgs.run_factor(v, x, s, P, metrics=False, ctx=ctx)
+            ok = out.ok and np.abs(out.r - ref.r).max() <= 1e-10 * np.abs(ref.r).max()
+        except Exception as e:  # noqa: BLE001
+            ok = False
+        if not ok:
+            bad.append((v, n, m, s, P, out.error[:60] if 'out' in dir() and not out.ok else ''))
+    del ctx
+print("BAD", bad)
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BGS_POISON="1")
+    r = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "BAD []" in r.stdout, r.stdout[-2000:]
