@@ -185,7 +185,10 @@ struct DBuf {
     CUDA_OK(cudaMalloc(&p, b));
     bytes = b;
     static const bool poison = getenv("BGS_POISON") != nullptr;  // tests: NaN-fill new buffers
-    if (poison) CUDA_OK(cudaMemset(p, 0xFF, b));
+    if (poison) {  // (completed before any stream of the context can touch the buffer)
+      CUDA_OK(cudaMemset(p, 0xFF, b));
+      CUDA_OK(cudaDeviceSynchronize());
+    }
   }
   void release() {
     if (p) cudaFree(p);
