@@ -679,3 +679,35 @@ print("BAD", bad)
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "BAD []" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_leading_dimensions(gpu_ctx, pinned):
+    """bgs_factor with host leading dimensions larger than n (ldx = n + 7, ldq = n + 3, ldr =
+    m + 2), from pageable and from pinned buffers: the same bits as run_factor's compact
+    layout, and the padding of Q and R untouched."""
+    import ctypes
+    import torch
+    from paper_2507_21791_b200 import api
+    import paper_2507_21791_b200 as bgs
+    n, m, s, v = 40001, 48, 4, 3
+    x = bgs.gen_gaussian_host(99, n, m)
+    ref = bgs.run_factor(v, x, s, 1, metrics=False, ctx=gpu_ctx)
+    ldx, ldq, ldr = n + 7, n + 3, m + 2
+    tx = torch.full((m, ldx), np.nan, dtype=torch.float64)
+    tx[:, :n] = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(x).T))
+    tq = torch.full((m, ldq), -7.0, dtype=torch.float64)
+    if pinned:
+        tx, tq = tx.pin_memory(), tq.pin_memory()
+    r = np.full((ldr, m), -5.0)  # row-major view of an ldr x m column-major block
+    st, tm, err = api._Stats(), api._Timing(), api._Err()
+    rc = api._lib.bgs_factor(gpu_ctx.handle, v, n, m, s, 1, tx.data_ptr(), ldx, tq.data_ptr(), ldq,
+                             r.ctypes.data, ldr, ctypes.byref(st), ctypes.byref(tm),
+                             ctypes.byref(err))
+    api._raise(rc, err)
+    q = tq.numpy()
+    assert np.array_equal(q[:, :n].T, ref.q)
+    assert np.all(q[:, n:] == -7.0)
+    rr = r.reshape(m, ldr)  # column j of R at rr[j, :m]
+    assert np.array_equal(rr[:, :m].T, ref.r)
+    assert np.all(rr[:, m:] == -5.0)
