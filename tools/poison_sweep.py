@@ -9,7 +9,8 @@ from oracle.oracle import Oracle
 o = Oracle()
 bad = []
 shapes = [(70001, 96, 4, 3), (3000, 800, 4, 1), (20001, 64, 4, 2), (4097, 64, 1, 1), (4097, 64, 2, 3),
-          (1500, 48, 6, 2), (6000, 160, 8, 1), (9001, 128, 16, 2)]
+          (1500, 48, 6, 2), (6000, 160, 8, 1), (9001, 128, 16, 2), (5003, 36, 4, 1), (7777, 44, 4, 2),
+          (3333, 30, 5, 1), (2222, 35, 7, 3), (12345, 52, 4, 1), (999, 60, 12, 2)]
 for (n, m, s, P) in shapes:
     x = o.gen_matrix(n, m, s, 1e3, 777, False)
     ctx = bgs.Context(0)
