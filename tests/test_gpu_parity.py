@@ -711,3 +711,16 @@ def test_host_leading_dimensions(gpu_ctx, pinned):
     rr = r.reshape(m, ldr)  # column j of R at rr[j, :m]
     assert np.array_equal(rr[:, :m].T, ref.r)
     assert np.all(rr[:, m:] == -5.0)
+
+
+def test_randomized_parity_fuzz():
+    """200 random (variant, n, m, s, procs, kappa, generator, seed) cases inside each
+    variant's working assumption against the oracle (tools/fuzz_parity.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "tools/fuzz_parity.py", "200", "2024"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "failures: 0" in r.stdout, r.stdout[-3000:]

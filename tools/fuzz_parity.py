@@ -1,0 +1,57 @@
+# Randomized parity fuzzing against the oracle: random (variant, n, m, s, procs, kappa,
+# seed) within each variant's working assumption u kappa^p <= 1e-3 (p = 1 BCGSI+ / P-2S,
+# 2 PIPI+ / P-1S, 3 BCGSI+1S; variant.cpp:88-104); R to 1e-10 (normwise), LOO / residual
+# within 10x, identical sync accounting.  Optional BGS_POISON=1.  Prints failures.
+#   python tools/fuzz_parity.py [count] [seed]
+import sys, time
+sys.path.insert(0, ".")
+import numpy as np
+import paper_2507_21791_b200 as bgs
+from oracle.oracle import Oracle
+U = 2.0 ** -53
+count = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+o = Oracle()
+ctx = bgs.Context(0)
+fails, t0 = [], time.time()
+for it in range(count):
+    v = int(rng.integers(1, 6))
+    s = int(rng.choice([1, 2, 3, 4, 4, 4, 5, 6, 8, 12, 16]))
+    q = int(rng.integers(1, 13))
+    m = s * q
+    n = int(m + rng.integers(0, int(rng.choice([64, 4000, 30000]))))
+    P = int(rng.choice([1, 1, 1, 2, 3, 5]))
+    kappa = float(10.0 ** rng.uniform(0, 6))
+    p = {1: 1, 2: 2, 3: 2, 4: 1, 5: 3}[v]
+    if U * kappa ** p > 1e-3:
+        continue
+    gauss = bool(rng.integers(0, 2))
+    seed = int(rng.integers(1, 10 ** 6))
+    x = o.gen_matrix(n, m, s, kappa, seed, gauss)
+    ref = o.factor(v, x, s, P, metrics=True)
+    if ref.rc != 0:
+        continue
+    try:
+        out = bgs.run_factor(v, x, s, P, metrics=False, ctx=ctx)
+    except Exception as e:  # noqa: BLE001
+        fails.append((it, v, n, m, s, P, kappa, gauss, seed, "EXC " + str(e)[:60]))
+        continue
+    why = []
+    if not out.ok:
+        why.append("abort " + out.error[:50])
+    else:
+        mx = np.abs(ref.r).max()
+        if np.abs(out.r - ref.r).max() > 1e-10 * mx:
+            why.append("R %.1e" % (np.abs(out.r - ref.r).max() / mx))
+        if out.stats.sync_count != ref.sync_count or out.stats.event_labels != ref.labels:
+            why.append("syncs")
+        loo, res = o.loo(out.q), o.residual(x, out.q, out.r)
+        if loo > 10 * max(ref.loo, U):
+            why.append("loo %.1e vs %.1e" % (loo, ref.loo))
+        if res > 10 * max(ref.resid, U):
+            why.append("res %.1e vs %.1e" % (res, ref.resid))
+    if why:
+        fails.append((it, v, n, m, s, P, kappa, gauss, seed, "; ".join(why)))
+print(f"{count} cases in {time.time() - t0:.0f} s; failures: {len(fails)}")
+for f in fails:
+    print("FAIL", f)
