@@ -3,6 +3,8 @@
 # 2 PIPI+ / P-1S, 3 BCGSI+1S; variant.cpp:88-104); R to 1e-10 (normwise), LOO / residual
 # within 10x, identical sync accounting.  Optional BGS_POISON=1.  Prints failures.
 #   python tools/fuzz_parity.py [count] [seed]
+# FUZZ_NCCL=1: through bgs_factor_device on a one-rank NCCL context (the collective path;
+# procs = 1) instead of bgs_factor.
 import sys, time
 sys.path.insert(0, ".")
 import numpy as np
@@ -12,7 +14,35 @@ U = 2.0 ** -53
 count = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 o = Oracle()
-ctx = bgs.Context(0)
+import os
+nccl = os.environ.get("FUZZ_NCCL") == "1"
+if nccl:
+    import torch
+    ctx = bgs.Context(0, 0, 1, bgs.nccl_unique_id())
+else:
+    ctx = bgs.Context(0)
+
+
+class _Out:
+    pass
+
+
+def factor_nccl(v, x, s):
+    n, m = x.shape
+    ld = (n + 31) // 32 * 32
+    X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    X[:, :n] = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(x).T)).cuda()
+    Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    out = _Out()
+    try:
+        r, st, tm = bgs.factor_device(ctx, v, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+        out.ok, out.error, out.r, out.stats = True, "", r, st
+        out.q = np.asfortranarray(Q[:, :n].cpu().numpy().T)
+    except bgs.api.NotSpdError as e:
+        out.ok, out.error = False, str(e)
+    return out
+
+
 fails, t0 = [], time.time()
 for it in range(count):
     v = int(rng.integers(1, 6))
@@ -20,7 +50,7 @@ for it in range(count):
     q = int(rng.integers(1, 13))
     m = s * q
     n = int(m + rng.integers(0, int(rng.choice([64, 4000, 30000]))))
-    P = int(rng.choice([1, 1, 1, 2, 3, 5]))
+    P = 1 if nccl else int(rng.choice([1, 1, 1, 2, 3, 5]))
     kappa = float(10.0 ** rng.uniform(0, 6))
     p = {1: 1, 2: 2, 3: 2, 4: 1, 5: 3}[v]
     if U * kappa ** p > 1e-3:
@@ -32,7 +62,7 @@ for it in range(count):
     if ref.rc != 0:
         continue
     try:
-        out = bgs.run_factor(v, x, s, P, metrics=False, ctx=ctx)
+        out = factor_nccl(v, x, s) if nccl else bgs.run_factor(v, x, s, P, metrics=False, ctx=ctx)
     except Exception as e:  # noqa: BLE001
         fails.append((it, v, n, m, s, P, kappa, gauss, seed, "EXC " + str(e)[:60]))
         continue
