@@ -32,6 +32,17 @@ def test_reference_arm_contract():
                         "d2h_bytes_per_step": 0}
 
 
+def test_reference_arm_nonzero_rank_is_silent():
+    """Under torchrun (N > 1) only rank 0 runs the reference arm; other ranks exit 0
+    without output or work."""
+    env = dict(os.environ, RANK="1", LOCAL_RANK="1", WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                        "--steps", "3", "--warmup", "3"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=120, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip() == ""
+
+
 @pytest.mark.gpu
 def test_gpu_arm_contract():
     d = run_bench("--n", "200000", "--m", "64", "--steps", "2", "--warmup", "3",
