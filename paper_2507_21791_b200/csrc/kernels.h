@@ -49,6 +49,8 @@ struct alignas(64) TileParams {
   unsigned long long* phase;  // BGS_TILE_PROF: per-CTA cycle counters [grid][8] (or null)
   int dbg;  // experiment mask (BGS_TILE_DBG): 1 no proxy fence, 2 no global stores,
             // 4 no update MMAs, 8 no Gram MMAs, 16 no epilogue
+  int comp_t0;  // first compensated output tile (>= mt_out: none; every 4-row k-step of
+                // tiles >= comp_t0 is folded into their double-double at once)
 };
 
 cudaError_t tile_launch(TileParams& p, bool upd, int grid, cudaStream_t st, int* launches);
@@ -97,6 +99,7 @@ struct alignas(64) SplitParams {
   unsigned long long* phase;
   int dbg;
   int pdl;              // launched as a programmatic dependent of the merged reduce + step
+  int comp_t0;          // first compensated output tile (>= mt_out: none; k12_ct.cu)
 };
 // Plans the rank split for a fused Gram of the given shape; false when K12c does not
 // apply (then the caller uses tile_launch).  Fills own/ext ranges, slot_units, stages.

@@ -373,7 +373,18 @@ struct GramSpec {
   int N = 0;
   int rspan[32];
   int rcol[32];
+  // Gram rows >= comp_row (compact row index) are accumulated with every 4-row k-step
+  // folded into a double-double (gram_ct.cu / k12_ct.cu): BCGSI+1S's U rows
+  int comp_row = 1 << 30;
 };
+// first compensated output tile of a Gram whose span 0 has lc0 output-row columns in
+// units0 8-column units (span-1 output rows follow at tile units0); mt_out: none
+static int comp_tile(const GramSpec& g, int lc0, int units0, int mt_out) {
+  const int r = g.comp_row;
+  if (r < 0 || r >= (1 << 30)) return mt_out;
+  const int t = r < lc0 ? r / 8 : units0 + (r - lc0) / 8;
+  return t < mt_out ? t : mt_out;
+}
 
 class Runner {
  public:
@@ -394,6 +405,7 @@ class Runner {
   int gram_max_units = 0;  // BGS_GRAM_MAXUNITS (tests): chunk unfused Grams above this
   bool no_merge_small = false;  // BGS_NO_MERGE_SMALL: separate reduce and small launches
   bool no_pdl = false;          // BGS_NO_PDL: no programmatic dependent launch of K12c
+  int comp_mode = 1;            // BGS_COMP_TAIL: 0 off, 1 BCGSI+1S (default), 2 all modes
   // Programmatic dependent launch of a fused kernel is allowed only right behind the
   // merged reduce + step kernel (nothing queued in between): that kernel writes only the
   // Gram, the small factors and the status word, which the fused kernel reads after its
@@ -418,6 +430,8 @@ class Runner {
     gram_max_units = e4 ? atoi(e4) : 0;
     const char* e5 = getenv("BGS_NO_MERGE_SMALL");
     no_merge_small = e5 && *e5 && *e5 != '0';
+    const char* ect = getenv("BGS_COMP_TAIL");
+    comp_mode = !ect ? 1 : (*ect == '0' ? 0 : (strcmp(ect, "all") == 0 ? 2 : 1));
     const char* e6 = getenv("BGS_NO_PDL");
     no_pdl = e6 && *e6 && *e6 != '0';
     const char* d = getenv("BGS_TILE_DBG");
@@ -593,6 +607,7 @@ class Runner {
     p.kp = kp;
     p.s = (int)s;
     if (!k12_plan(p)) return false;
+    p.comp_t0 = comp_tile(sp, sp.sp[0].ncols, p.U0, p.mt_out);
     for (auto& x : sh)
       if (x.rows > 0 && grid_for(x) < p.cluster) return false;
     return true;
@@ -750,6 +765,7 @@ class Runner {
         const int len = std::min(cw, r.n - c0);
         GramSpec g = spec2(r.src, r.col0 + c0, len, len, SR, 0, N, 0);
         add_right(g, 1, 0, N);
+        if (sp.comp_row < row_off + len) g.comp_row = std::max(0, sp.comp_row - row_off);
         gout = c->G.d() + row_off;
         gout_ld = M;
         gram(g, "", false, false);
@@ -790,6 +806,7 @@ class Runner {
       p.col0[i] = sp.sp[i].col0;
       p.lcols[i] = lc[i];
     }
+    p.comp_t0 = comp_tile(sp, lc[0], units[0], p.mt_out);
     for (int j = 0; j < 32; ++j)
       p.rcol[j] = j < sp.N ? (sp.rspan[j] == 0 ? sp.rcol[j] : 8 * units[0] + sp.rcol[j]) : -1;
     p.status = status;
@@ -1054,7 +1071,14 @@ class Runner {
       g = spec1(SQ, 0, kp + si, kp + si);
       add_right(g, 0, kp, si);
     }
+    if (comp_tail(mode)) g.comp_row = kp;  // U_j in Q block j
     return g;
+  }
+  // BCGSI+1S carries U unnormalized: its Gram rows U^T [U X] feed Y_diag = chol(Omega -
+  // Y^T Y) and S2 directly, so they get the compensated accumulation (DESIGN.md
+  // "Numerics").  BGS_COMP_TAIL=0: off; =all: every one-sync mode (experiments).
+  bool comp_tail(int mode) const {
+    return comp_mode == 2 || (comp_mode == 1 && mode == OS_SKIP);
   }
   // The same Gram on the tile of a fused update: Q_{1:j} in span 0, [X_j -> U_j, X_{j+1}]
   // in span 1 (U_j produced in place by the update).
@@ -1065,6 +1089,7 @@ class Runner {
                        (wide && mode == OS_PYTH) ? 2 * si : si);
     add_right(g, 1, 0, si);
     if (wide) add_right(g, 1, si, si);
+    if (comp_tail(mode)) g.comp_row = kp;  // U_j: the first span-1 output row
     return g;
   }
 
@@ -1157,6 +1182,7 @@ class Runner {
       const char* lab = k + 2 < q ? "fused_gram:wide" : "fused_gram:final";
       GramSpec gf = onesync_spec_fused(mode, k + 1);
       gf.sp[0].ncols = gf.sp[0].lcols = kp + si;  // span 0 = [Q_{1:k} | U_k -> Q_k]
+      if (comp_tail(mode)) gf.comp_row = kp + si;  // U_{k+1}: span 1
       // (span 1 still starts at X block k+1)
       if (fusable && fuse_ok(gf, kp)) {
         Fuse fz;
