@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU seconds of one reference sample run")
+    ap.add_argument("--ref-full", action="store_true",
+                    help="--impl reference: time the whole workload once (no row sample)")
     a = ap.parse_args()
     if a.config == 1:
         a.n, a.m, a.s, a.dist = 100_000, 64, 4, "gaussian"
@@ -203,37 +205,61 @@ def ncu_traffic(kernel):
 # ---------------------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------------------
+# VariantId order and canonical names of the reference (variant.hpp:8-15,
+# variant.cpp:18-34); the reference arm resolves --variant with this table, not with our
+# package (nothing of the product is loaded on this arm).
+REF_VARIANTS = ["BCGS", "BCGSI+", "BCGSPIPI+", "BCGSI+P-1S", "BCGSI+P-2S", "BCGSI+1S"]
+
+
 def run_reference_arm(a):
+    """The reference's own CPU implementation (oracle/_ref, compiled from /root/reference
+    by oracle/Makefile; the C port when it is absent) on this box's host cores, through
+    its run_variant under run_spmd.  Each step is a bounded row sample of the workload
+    (cost and flops are both linear in n); `value` is the measured GFLOP/s of those
+    samples, `ms_per_step` their measured mean time -- nothing is extrapolated.
+    --ref-full times the whole workload instead (config 2: ~6 min on 16 threads)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    import paper_2507_21791_b200 as bgs
-    v = bgs.parse_variant(a.variant)
+    from oracle.oracle import Oracle, Reference
+    names = [x.upper() for x in REF_VARIANTS]
+    if a.variant.upper() not in names:
+        print(json.dumps({"impl": "reference", "unavailable": f"unknown variant {a.variant}"}))
+        return 0
+    v = names.index(a.variant.upper())
+    counter = Reference() if Reference.available() else Oracle()
     per_step = max(2.0, a.cpu_seconds * 8.0 / max(8, a.steps + a.warmup))
-    kind, cores, run = cpu_reference_runner(int(v), a.n, a.m, a.s, a.seed, a.dist == "gaussian",
+    kind, cores, run = cpu_reference_runner(v, a.n, a.m, a.s, a.seed, a.dist == "gaussian",
                                             a.kappa)
-    rows, _ = pick_sample_rows(run, a.n, a.m, per_step)
-    for _ in range(a.warmup):
+    if a.ref_full:
+        rows = a.n
+        warm, steps = 0, 1
+    else:
+        rows, _ = pick_sample_rows(run, a.n, a.m, per_step)
+        warm, steps = a.warmup, a.steps
+    for _ in range(warm):
         run(rows)
-    secs = [run(rows) for _ in range(a.steps)]
+    secs = [run(rows) for _ in range(steps)]
     t = sum(secs) / len(secs)
-    flops = bgs.variant_flops(int(v), rows, a.m, a.s)
+    flops = counter.variant_flops(v, rows, a.m, a.s)  # cost_model.cpp:29-119
     gf = flops / t / 1e9
-    sample = (f"{a.variant} n={rows} m={a.m} s={a.s} {dist_text(a)} (row subsample of the workload; "
-              f"cost and flops both scale with n), {'reference library oracle/_ref' if kind == 'reference' else 'oracle port'} "
-              f"run_variant under run_spmd with P={cores} threads, mean of {a.steps} runs")
+    what = "the whole workload" if rows == a.n else "a row sample of the workload"
+    sample = (f"{a.variant} n={rows} m={a.m} s={a.s} {dist_text(a)} ({what}; cost and flops "
+              f"both linear in n), {'reference library oracle/_ref' if kind == 'reference' else 'oracle C port'} "
+              f"run_variant under run_spmd with P={cores} threads, mean of {steps} timed runs "
+              f"after {warm} warm-up runs")
     line = {
         "impl": "reference", "metric": metric_name(a), "value": gf, "unit": "GFLOP/s",
-        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": t * 1e3 * (a.n / rows), "higher_is_better": True, "scaling": "strong",
+        "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded {dist_text(a)}, reference gen_matrix)",
         "config": workload_config(a, world),
+        "sample_rows": rows,
         "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "ms_per_step extrapolated to the full n from the sample (cost is linear in n)",
     }
     print(json.dumps(line), flush=True)
     return 0

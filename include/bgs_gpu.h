@@ -8,7 +8,8 @@
  *
  * Compute runs on hand-written sm_100a kernels (TMA + DMMA Gram, fused block update,
  * on-device small factor ops, on-device TSQR); the single synchronization of each block
- * step is one NCCL allreduce when the context spans several GPUs.  There is no CPU
+ * step is one NCCL allreduce when the context spans several GPUs (or one exchange through
+ * a caller-supplied host communicator, bgs_ctx_create_host_comm).  There is no CPU
  * fallback: on a host without a usable B200 every compute entry point returns
  * BGS_E_CUDA.
  */
@@ -93,6 +94,18 @@ int bgs_shard_rows(long n, int procs, int rank, long* row0, long* rows); /* dist
  * by all ranks. */
 int bgs_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
                    bgs_ctx** out, bgs_error* err);
+/* A context whose collectives go through a caller-supplied host communicator instead of
+ * NCCL -- the reference's Communicator (communicator.hpp:98-152) as a callback.  `fn` is
+ * a blocking allgather: every rank passes `bytes` bytes in `send` and receives all ranks'
+ * buffers in rank order in `recv` (nranks * bytes); it returns 0 on success.  Each sync
+ * of the algorithm (a Gram allreduce, a TSQR root exchange with its fused Gram) is ONE
+ * call: the partials are gathered and summed in rank order on the host, so R is bitwise
+ * replicated (exact_allreduce, communicator.cpp:226-250).  Uses: ranks that share a GPU
+ * (tests: several processes on one device, where NCCL refuses), or a transport NCCL does
+ * not cover.  No kernel ever waits on another rank: the exchange is between launches. */
+typedef int (*bgs_allgather_fn)(void* user, const void* send, void* recv, unsigned long bytes);
+int bgs_ctx_create_host_comm(int device, int rank, int nranks, bgs_allgather_fn fn, void* user,
+                             bgs_ctx** out, bgs_error* err);
 void bgs_ctx_destroy(bgs_ctx* ctx);
 int bgs_nccl_unique_id(void* out128, bgs_error* err); /* ncclGetUniqueId via the ctx's NCCL */
 /* The *_device entry points below run on the context's own stream and first wait (an
@@ -101,6 +114,23 @@ int bgs_nccl_unique_id(void* out128, bgs_error* err); /* ncclGetUniqueId via the
  * (torch's default).  `stream` is a cudaStream_t.  Results are complete on return. */
 int bgs_ctx_set_stream(bgs_ctx* ctx, void* stream);
 int bgs_device_info(int device, int* sm_count, long* hbm_bytes, char* name, long name_cap);
+
+/* ---- BcgsOptions (bcgs.hpp:19-30) ---------------------------------------------------
+ * `probe` is RecurrenceProbe::on_eval: the one-sync variants (BCGSI+P-1S, BCGSI+P-2S,
+ * BCGSI+1S) call it once per delayed reprojection (bcgs.cpp:339-343) with the 1-based
+ * block index k of Q_k, the s x s recurrence S2 (column-major, host), and this shard's
+ * rows of Q_k and X_{k+1} (host copies, n_local x s, ld n_local), so a test can form the
+ * never-communicated product Q_k^T X_{k+1} directly.  `shard` is the rank (the emulated
+ * shard under bgs_factor with procs > 1).  Firing it synchronizes the stream once per
+ * step (a debugging hook, like the reference's).  classic_intra is accepted for API
+ * parity; classic BCGS is out of scope, so it has no effect. */
+typedef void (*bgs_probe_fn)(void* user, long k, const double* s2, long s, const double* q_local,
+                             const double* x_local, long n_local, int shard);
+typedef struct {
+  int classic_intra; /* IntraorthKind: 0 Tsqr (default), 1 CholQr -- unused on this path */
+  bgs_probe_fn probe;
+  void* probe_user;
+} bgs_options;
 
 /* ---- drop-in for run_factor (runner.hpp:28-29, runner.cpp:39-67) ------------------
  * Host X (n x m, ldx) in; Q (n x m, ldq, gathered in rank order like gather_rows) and
@@ -112,6 +142,11 @@ int bgs_device_info(int device, int* sm_count, long* hbm_bytes, char* name, long
 int bgs_factor(bgs_ctx* ctx, int variant, long n, long m, long s, int procs,
                const double* x, long ldx, double* q, long ldq, double* r, long ldr,
                bgs_stats* stats, bgs_timing* timing, bgs_error* err);
+/* run_factor(v, x, s, procs, opts): the same with BcgsOptions (opts may be NULL). */
+int bgs_factor_opts(bgs_ctx* ctx, int variant, long n, long m, long s, int procs,
+                    const double* x, long ldx, double* q, long ldq, double* r, long ldr,
+                    const bgs_options* opts, bgs_stats* stats, bgs_timing* timing,
+                    bgs_error* err);
 
 /* ---- device-resident per-rank entry (run_variant on a DistBlockMatrix,
  * bcgs.hpp:49-50).  This rank owns rows [row0, row0 + n_local) of the global n x m
@@ -124,6 +159,11 @@ int bgs_factor_device(bgs_ctx* ctx, int variant, long n, long m, long s, long ro
                       long n_local, const double* d_x, long ldx, double* d_q, long ldq,
                       double* h_r, long ldr, bgs_stats* stats, bgs_timing* timing,
                       bgs_error* err);
+/* run_variant(v, x, comm, opts) (bcgs.hpp:49-50): the same with BcgsOptions. */
+int bgs_factor_device_opts(bgs_ctx* ctx, int variant, long n, long m, long s, long row0,
+                           long n_local, const double* d_x, long ldx, double* d_q, long ldq,
+                           double* h_r, long ldr, const bgs_options* opts, bgs_stats* stats,
+                           bgs_timing* timing, bgs_error* err);
 
 /* ---- inputs and verification on the device (matrix_gen.hpp:27, metrics.hpp:10-20) -- */
 /* Seeded i.i.d. N(0,1) entries X(i,j) for global rows [row0, row0+n_local): a

@@ -182,6 +182,13 @@ class Reference:
             out.loo, out.resid = loo.value, res.value
         return out
 
+    def variant_flops(self, v, n, m, s):
+        """cost_model.cpp:29-119 (the reference's own analytic count)."""
+        return self.lib.ref_variant_flops(v, n, m, s)
+
+    def expected_syncs(self, v, q):
+        return self.lib.ref_expected_syncs(v, q)
+
     def gram(self, a, b):
         a, b = _f(a), _f(b)
         out = np.zeros((a.shape[1], b.shape[1]), order="F")

@@ -6,14 +6,14 @@ include/bgs_gpu.h, mirrored here with the reference's names (see api.py).
 """
 from .api import *  # noqa: F401,F403
 from .api import (  # noqa: F401
-    Context, FactorOutcome, SyncStats, VariantId, all_variants, default_context,
+    BcgsOptions, Context, FactorOutcome, SyncStats, VariantId, all_variants, default_context,
     expected_syncs, factor_device, gen_gaussian_device, gen_gaussian_host, gram,
     loss_and_residual, metrics_device, nccl_unique_id, parse_variant, run_factor, shard_rows,
     tsqr, variant_flops, variant_name,
 )
 
 __all__ = [
-    "Context", "FactorOutcome", "SyncStats", "VariantId", "all_variants", "default_context",
+    "BcgsOptions", "Context", "FactorOutcome", "SyncStats", "VariantId", "all_variants", "default_context",
     "expected_syncs", "factor_device", "gen_gaussian_device", "gen_gaussian_host", "gram",
     "loss_and_residual", "metrics_device", "nccl_unique_id", "parse_variant", "run_factor",
     "shard_rows", "tsqr", "variant_flops", "variant_name",

@@ -8,6 +8,7 @@ Names, argument meaning and error behaviour follow the reference headers
 * ``variant_flops`` — cost_model.hpp:37 / cost_model.cpp:29-119
 * ``SyncStats`` — sync_stats.hpp:13-27
 * ``FactorOutcome`` / ``run_factor`` — runner.hpp:11-29 / runner.cpp:39-67
+* ``BcgsOptions`` (probe = RecurrenceProbe) — bcgs.hpp:19-30
 * ``gram``, ``tsqr`` — dense_kernels.hpp:15-24, intraorth.hpp:22-27 (building blocks)
 * the exception taxonomy — errors.hpp:9-51
 
@@ -22,7 +23,7 @@ import enum
 import os
 import sys
 from dataclasses import dataclass, field
-from typing import Dict, List, Optional
+from typing import Callable, Dict, List, Optional
 
 import numpy as np
 
@@ -158,6 +159,9 @@ def _load() -> ctypes.CDLL:
         "bgs_profile_enable": ([P, I], I),
         "bgs_profile_read": ([P, P, I, P], I),
         "bgs_tsqr": ([P, P, L, L, P, P, P], I),
+        "bgs_ctx_create_host_comm": ([I, I, I, P, P, P, P], I),
+        "bgs_factor_opts": ([P, I, L, L, L, I, P, L, P, L, P, L, P, P, P, P], I),
+        "bgs_factor_device_opts": ([P, I, L, L, L, L, L, P, L, P, L, P, L, P, P, P, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -174,8 +178,20 @@ EXPORTED_SYMBOLS = (
     "bgs_nccl_unique_id",
     "bgs_device_info", "bgs_factor", "bgs_factor_device", "bgs_gen_gaussian_device",
     "bgs_gen_gaussian_host", "bgs_metrics", "bgs_metrics_device", "bgs_gram", "bgs_tsqr",
-    "bgs_profile_enable", "bgs_profile_read",
+    "bgs_profile_enable", "bgs_profile_read", "bgs_ctx_create_host_comm", "bgs_factor_opts",
+    "bgs_factor_device_opts",
 )
+
+# bgs_allgather_fn / bgs_probe_fn (include/bgs_gpu.h)
+_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_ulong)
+_PROBE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_long, ctypes.POINTER(ctypes.c_double),
+                             ctypes.c_long, ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(ctypes.c_double), ctypes.c_long, ctypes.c_int)
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("classic_intra", ctypes.c_int), ("probe", _PROBE_FN), ("probe_user", ctypes.c_void_p)]
 
 
 def _raise(rc: int, err: _Err) -> None:
@@ -293,17 +309,39 @@ class FactorOutcome:
 
 class Context:
     """A device + stream (+ NCCL communicator when nranks > 1, or when an id is given for a
-    one-rank context) + workspaces."""
+    one-rank context) + workspaces.
+
+    ``host_allgather``: instead of NCCL, a blocking host allgather ``f(bytes) -> bytes``
+    (every rank's payload concatenated in rank order), e.g. over torch.distributed gloo
+    (``dist.host_allgather``).  Each sync is one call; partials are summed in rank order
+    on the host (bgs_ctx_create_host_comm).  Lets several ranks share one GPU."""
 
     def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1,
-                 nccl_unique_id: Optional[bytes] = None):
+                 nccl_unique_id: Optional[bytes] = None,
+                 host_allgather: Optional[Callable[[bytes], bytes]] = None):
         self._h = ctypes.c_void_p()
         err = _Err()
-        uid = None
-        if nccl_unique_id is not None:
-            uid = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
-        rc = _lib.bgs_ctx_create(int(device), int(rank), int(nranks), uid,
-                                 ctypes.byref(self._h), ctypes.byref(err))
+        self._cb = None
+        if host_allgather is not None:
+            def _ag(user, send, recv, nbytes, _f=host_allgather, _p=int(nranks)):
+                try:
+                    out = _f(ctypes.string_at(send, nbytes))
+                    if len(out) != _p * nbytes:
+                        return 1
+                    ctypes.memmove(recv, out, len(out))
+                    return 0
+                except Exception:  # noqa: BLE001  (reported as BGS_E_COLLECTIVE)
+                    return 1
+            self._cb = _ALLGATHER_FN(_ag)
+            rc = _lib.bgs_ctx_create_host_comm(int(device), int(rank), int(nranks),
+                                               ctypes.cast(self._cb, ctypes.c_void_p), None,
+                                               ctypes.byref(self._h), ctypes.byref(err))
+        else:
+            uid = None
+            if nccl_unique_id is not None:
+                uid = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+            rc = _lib.bgs_ctx_create(int(device), int(rank), int(nranks), uid,
+                                     ctypes.byref(self._h), ctypes.byref(err))
         _raise(rc, err)
         self.device, self.rank, self.nranks = device, rank, nranks
 
@@ -383,8 +421,39 @@ def _ptr(a: np.ndarray) -> int:
 # ---------------------------------------------------------------------------------------
 
 
+@dataclass
+class BcgsOptions:
+    """BcgsOptions (bcgs.hpp:25-30).  ``probe(k, s2, q_local, x_local, shard)`` is
+    RecurrenceProbe::on_eval: called once per delayed reprojection of the one-sync variants
+    with the 1-based index k of Q_k, the s x s recurrence S2 and this shard's rows of Q_k
+    and X_{k+1} (numpy copies)."""
+    classic_intra: int = 0
+    probe: Optional[Callable[[int, np.ndarray, np.ndarray, np.ndarray, int], None]] = None
+
+
+def _options(opts: Optional[BcgsOptions]):
+    """(ctypes _Options or None, keep-alive) for a call."""
+    if opts is None:
+        return None, None
+    o = _Options()
+    o.classic_intra = int(opts.classic_intra)
+    cb = None
+    if opts.probe is not None:
+        def _pr(user, k, s2, s, ql, xl, nl, shard, _f=opts.probe):
+            sq = np.ctypeslib.as_array(s2, shape=(s * s,)).reshape((s, s), order="F").copy()
+            q = (np.ctypeslib.as_array(ql, shape=(nl * s,)).reshape((nl, s), order="F").copy()
+                 if nl else np.zeros((0, s)))
+            xx = (np.ctypeslib.as_array(xl, shape=(nl * s,)).reshape((nl, s), order="F").copy()
+                  if nl else np.zeros((0, s)))
+            _f(int(k), sq, q, xx, int(shard))
+        cb = _PROBE_FN(_pr)
+        o.probe = cb
+    return o, cb
+
+
 def run_factor(v: int, x: np.ndarray, s: int, procs: int = 1, *, metrics: bool = True,
-               ctx: Optional[Context] = None) -> FactorOutcome:
+               ctx: Optional[Context] = None, opts: Optional[BcgsOptions] = None
+               ) -> FactorOutcome:
     """Distribute x over `procs` ranks (emulated on one device), factor, gather, measure.
 
     NotSpd becomes ``ok=False`` with the diagnostic preserved (runner.cpp:56-61); every
@@ -398,9 +467,11 @@ def run_factor(v: int, x: np.ndarray, s: int, procs: int = 1, *, metrics: bool =
     q = np.zeros((n, m), dtype=np.float64, order="F")
     r = np.zeros((m, m), dtype=np.float64, order="F")
     st, tm, err = _Stats(), _Timing(), _Err()
-    rc = _lib.bgs_factor(ctx.handle, int(v), n, m, int(s), int(procs), _ptr(xf), max(n, 1),
-                         _ptr(q), max(n, 1), _ptr(r), max(m, 1), ctypes.byref(st),
-                         ctypes.byref(tm), ctypes.byref(err))
+    o, _keep = _options(opts)
+    rc = _lib.bgs_factor_opts(ctx.handle, int(v), n, m, int(s), int(procs), _ptr(xf), max(n, 1),
+                              _ptr(q), max(n, 1), _ptr(r), max(m, 1),
+                              ctypes.byref(o) if o is not None else None, ctypes.byref(st),
+                              ctypes.byref(tm), ctypes.byref(err))
     out = FactorOutcome()
     if rc == 2:
         out.ok = False
@@ -475,14 +546,16 @@ def gen_gaussian_host(seed: int, n: int, m: int) -> np.ndarray:
 
 
 def factor_device(ctx: Context, v: int, n: int, m: int, s: int, row0: int, n_local: int,
-                  x_ptr: int, ldx: int, q_ptr: int, ldq: int
-                  ) -> tuple[np.ndarray, SyncStats, Timing]:
+                  x_ptr: int, ldx: int, q_ptr: int, ldq: int,
+                  opts: Optional[BcgsOptions] = None) -> tuple[np.ndarray, SyncStats, Timing]:
     r = np.zeros((m, m), dtype=np.float64, order="F")
     st, tm, err = _Stats(), _Timing(), _Err()
     ctx._follow_torch()
-    rc = _lib.bgs_factor_device(ctx.handle, int(v), n, m, s, row0, n_local, x_ptr, ldx, q_ptr,
-                                ldq, _ptr(r), m, ctypes.byref(st), ctypes.byref(tm),
-                                ctypes.byref(err))
+    o, _keep = _options(opts)
+    rc = _lib.bgs_factor_device_opts(ctx.handle, int(v), n, m, s, row0, n_local, x_ptr, ldx,
+                                     q_ptr, ldq, _ptr(r), m,
+                                     ctypes.byref(o) if o is not None else None,
+                                     ctypes.byref(st), ctypes.byref(tm), ctypes.byref(err))
     _raise(rc, err)
     return r, SyncStats._from(st), Timing(tm.factor_ms, tm.total_ms, int(tm.kernel_launches))
 

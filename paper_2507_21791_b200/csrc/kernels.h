@@ -157,6 +157,7 @@ struct SmallParams {
   const double* aux2; int ldaux2; // IRO: R2
   double* save; int ldsave;       // where SM_IRO_SAVE / SM_PIPI_PROJ keep S
   DevStatus* status;
+  int unstaged;                   // set by small_launch: operands too large for shared memory
 };
 cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches);
 // gram_reduce followed by the s <= 4 one-sync step in one launch (single-GPU contexts: the

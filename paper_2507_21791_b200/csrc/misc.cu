@@ -85,24 +85,34 @@ cudaError_t copy_cols_launch(const double* src, long lds, double* dst, long ldd,
 // One thread per row and a 16-column tile of R held in shared memory:
 // d_ij = x_ij - sum_{k <= j} q_ik r_kj.  Partial sums of d^2 and x^2 per CTA, in
 // double-double, reduced by a second tiny kernel in fixed order.
+// SM = false (m > 1600: the tile does not fit shared memory): R is read from global
+// memory (L1 / L2 resident) instead.
 constexpr int RES_TILE = 16;
+template <bool SM>
 __global__ void __launch_bounds__(256)
     residual_kernel(const double* __restrict__ x, long ldx, const double* __restrict__ q, long ldq,
                     const double* __restrict__ r, long ldr, long n_rows, long m,
                     double2* __restrict__ part) {
-  extern __shared__ double rt[];  // (m) x RES_TILE
+  extern __shared__ double rt_sm[];  // (m) x RES_TILE
   __shared__ double red[2][8][2];
   double sd = 0.0, ed = 0.0, sx = 0.0, ex = 0.0;
   for (long j0 = 0; j0 < m; j0 += RES_TILE) {
     const int nj = (int)((m - j0) < RES_TILE ? (m - j0) : RES_TILE);
     const long kmax = j0 + nj;  // R upper: rows k < j0 + nj matter
-    __syncthreads();
-    for (long e = threadIdx.x; e < kmax * RES_TILE; e += blockDim.x) {
-      const long k = e % kmax;
-      const int jj = (int)(e / kmax);
-      rt[e] = jj < nj ? r[k + (size_t)(j0 + jj) * ldr] : 0.0;
+    if (SM) {
+      __syncthreads();
+      for (long e = threadIdx.x; e < kmax * RES_TILE; e += blockDim.x) {
+        const long k = e % kmax;
+        const int jj = (int)(e / kmax);
+        rt_sm[e] = jj < nj ? r[k + (size_t)(j0 + jj) * ldr] : 0.0;
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    // tile element (k, jj): shared copy, or R itself (columns past nj read as zero)
+    auto rt = [&](long k, int jj) -> double {
+      if (SM) return rt_sm[k + jj * kmax];
+      return jj < nj ? __ldg(&r[k + (size_t)(j0 + jj) * ldr]) : 0.0;
+    };
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n_rows;
          i += (long)gridDim.x * blockDim.x) {
       double acc[RES_TILE];
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(256)
       for (long k = 0; k < kmax; ++k) {
         const double qv = q[i + (size_t)k * ldq];
 #pragma unroll
-        for (int jj = 0; jj < RES_TILE; ++jj) acc[jj] = fma(qv, rt[k + jj * kmax], acc[jj]);
+        for (int jj = 0; jj < RES_TILE; ++jj) acc[jj] = fma(qv, rt(k, jj), acc[jj]);
       }
 #pragma unroll
       for (int jj = 0; jj < RES_TILE; ++jj) {
@@ -167,13 +177,18 @@ cudaError_t residual_launch(const double* x, long ldx, const double* q, long ldq
                             const double* r, long ldr, long n_rows, long m, double, double,
                             double* ws, double* out, int num_sms, cudaStream_t st) {
   const size_t smem = (size_t)m * RES_TILE * sizeof(double);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  ensure_smem(residual_kernel, smem);
   long grid = (n_rows + 255) / 256;
   if (grid > num_sms * 2) grid = num_sms * 2;
   if (grid < 1) grid = 1;
-  residual_kernel<<<(int)grid, 256, smem, st>>>(x, ldx, q, ldq, r, ldr, n_rows, m,
-                                                reinterpret_cast<double2*>(ws));
+  if (smem <= 200 * 1024) {
+    cudaError_t e = ensure_smem(residual_kernel<true>, smem);
+    if (e != cudaSuccess) return e;
+    residual_kernel<true><<<(int)grid, 256, smem, st>>>(x, ldx, q, ldq, r, ldr, n_rows, m,
+                                                        reinterpret_cast<double2*>(ws));
+  } else {
+    residual_kernel<false><<<(int)grid, 256, 0, st>>>(x, ldx, q, ldq, r, ldr, n_rows, m,
+                                                       reinterpret_cast<double2*>(ws));
+  }
   dd_finish_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const double2*>(ws), (int)grid, out);
   return cudaGetLastError();
 }

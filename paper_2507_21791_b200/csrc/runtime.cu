@@ -177,6 +177,24 @@ CUtensorMap make_map3(const double* base, long rows, long cols, long ld, int H, 
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }  // temporaries are freed on every exit path (Fail included)
   void ensure(size_t b) {
     if (b <= bytes) return;
     if (p) cudaFree(p);
@@ -203,6 +221,9 @@ struct DBuf {
 struct HBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  HBuf() = default;
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
   void ensure(size_t b) {
     if (b <= bytes) return;
     if (p) cudaFreeHost(p);
@@ -242,6 +263,11 @@ struct bgs_ctx {
   int device = 0, rank = 0, nranks = 1, sms = 148;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  // caller-supplied host communicator (bgs_ctx_create_host_comm): one allgather per sync
+  bgs_allgather_fn hc_fn = nullptr;
+  void* hc_user = nullptr;
+  HBuf hc_send, hc_recv, hc_out;
+  bool collective() const { return comm != nullptr || hc_fn != nullptr; }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   // The device-pointer entry points run on `stream` (non-blocking) but first wait for the
   // caller's work issued so far on `caller` (legacy default stream unless set with
@@ -392,9 +418,10 @@ class Runner {
   int variant;
   long n, m, s, q;
   int P;        // ranks of the factorization
-  bool use_nccl;
+  bool use_coll;  // a multi-rank (or one-rank NCCL) context: collectives between launches
   std::vector<Shard> sh;
   bgs_stats* stats;
+  const bgs_options* opt;  // BcgsOptions (probe)
   long words = 0;
   DevStatus* status;
   int tsqr_L = 0;  // total leaves across local shards
@@ -417,8 +444,8 @@ class Runner {
   int tile_dbg = 0;
   bool tile_prof = false;
 
-  Runner(bgs_ctx* ctx, int v, long n_, long m_, long s_, int P_, bool nccl_, bgs_stats* st)
-      : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_nccl(nccl_), stats(st) {
+  Runner(bgs_ctx* ctx, int v, long n_, long m_, long s_, int P_, bool nccl_, bgs_stats* st, const bgs_options* opt_ = nullptr)
+      : c(ctx), variant(v), n(n_), m(m_), s(s_), q(m_ / s_), P(P_), use_coll(nccl_), stats(st), opt(opt_) {
     const char* e = getenv("BGS_NO_FUSE");
     no_fuse = e && *e && *e != '0';
     // K12c (k12.cu) is the fused path; BGS_K12C=0 falls back to the single-CTA K12
@@ -575,6 +602,76 @@ class Runner {
     return g;
   }
 
+  // ---------------- collectives (between launches; no kernel waits on a rank) ----------
+  // Sum of every rank's n doubles at d (in place), identical bits on every rank.
+  void allreduce(double* d, size_t n) {
+    if (c->comm) {
+      Prof pr(c, "nccl_allreduce", (double)n * 8.0, 0.0);
+      NCCL_OK(nccl().AllReduce(d, d, n, ncclDouble, ncclSum, c->comm, c->stream));
+      return;
+    }
+    exchange(nullptr, 0, nullptr, d, n);
+  }
+  // One sync: allgather of ng doubles (send -> recv, rank-major) and allreduce of ns
+  // doubles at sum (in place).  NCCL: one group.  Host communicator: one allgather of the
+  // packed [gather | partial] buffer, the partials summed in rank order on the host.
+  void exchange(const double* send, size_t ng, double* recv, double* sum, size_t ns) {
+    if (c->comm) {
+      NCCL_OK(nccl().GroupStart());
+      if (ng) NCCL_OK(nccl().AllGather(send, recv, ng, ncclDouble, c->comm, c->stream));
+      if (ns) NCCL_OK(nccl().AllReduce(sum, sum, ns, ncclDouble, ncclSum, c->comm, c->stream));
+      NCCL_OK(nccl().GroupEnd());
+      return;
+    }
+    if (!c->hc_fn) fail(BGS_E_INTERNAL, "collective on a context without a communicator");
+    flush_reduce();
+    Prof pr(c, "host_exchange", (double)(ng + ns) * 8.0 * P, 0.0);
+    const size_t w = ng + ns;
+    c->hc_send.ensure(w * sizeof(double) + 64);
+    c->hc_recv.ensure((size_t)P * w * sizeof(double) + 64);
+    c->hc_out.ensure(((size_t)P * ng + ns) * sizeof(double) + 64);
+    double* hs = c->hc_send.d();
+    if (ng) CUDA_OK(cudaMemcpyAsync(hs, send, ng * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (ns) CUDA_OK(cudaMemcpyAsync(hs + ng, sum, ns * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));  // (also retires the previous exchange's H2D)
+    double* hr = c->hc_recv.d();
+    if (c->hc_fn(c->hc_user, hs, hr, (unsigned long)(w * sizeof(double))) != 0)
+      fail(BGS_E_COLLECTIVE, "host communicator allgather failed (rank %d of %d)", c->rank, P);
+    double* ho = c->hc_out.d();
+    for (int r = 0; r < P; ++r) memcpy(ho + (size_t)r * ng, hr + (size_t)r * w, ng * sizeof(double));
+    for (size_t i = 0; i < ns; ++i) {
+      double acc = hr[ng + i];
+      for (int r = 1; r < P; ++r) acc += hr[(size_t)r * w + ng + i];  // rank order
+      ho[(size_t)P * ng + i] = acc;
+    }
+    if (ng) CUDA_OK(cudaMemcpyAsync(recv, ho, (size_t)P * ng * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (ns) CUDA_OK(cudaMemcpyAsync(sum, ho + (size_t)P * ng, ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+
+  // RecurrenceProbe::on_eval (bcgs.cpp:339-343): S2 of step k and this rank's rows of Q_k
+  // (block k, final once the update of step k has run) and X_{k+1}, as host copies.
+  void fire_probe(long k, const double* s2_dev, int ld_s2) {
+    if (!opt || !opt->probe) return;
+    flush_reduce();
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+    std::vector<double> s2((size_t)s * s);
+    CUDA_OK(cudaMemcpy2D(s2.data(), s * sizeof(double), s2_dev, (size_t)ld_s2 * sizeof(double),
+                         s * sizeof(double), s, cudaMemcpyDeviceToHost));
+    for (size_t t = 0; t < sh.size(); ++t) {
+      const Shard& x = sh[t];
+      const long nl = std::max<long>(x.rows, 0);
+      std::vector<double> ql((size_t)nl * s + 1), xl((size_t)nl * s + 1);
+      if (nl) {
+        CUDA_OK(cudaMemcpy2D(ql.data(), nl * sizeof(double), x.Q + (size_t)(k * s) * x.ldq,
+                             x.ldq * sizeof(double), nl * sizeof(double), s, cudaMemcpyDeviceToHost));
+        CUDA_OK(cudaMemcpy2D(xl.data(), nl * sizeof(double), x.X + (size_t)((k + 1) * s) * x.ldx,
+                             x.ldx * sizeof(double), nl * sizeof(double), s, cudaMemcpyDeviceToHost));
+      }
+      opt->probe(opt->probe_user, k + 1, s2.data(), s, ql.data(), xl.data(), nl,
+                 use_coll ? c->rank : (int)t);
+    }
+  }
+
   // ---------------- K1 / K12 + reduction + (NCCL) allreduce ----------------
   // Fused block update carried in front of the Gram (K12); dst columns are Q columns.
   struct Fuse {
@@ -676,11 +773,7 @@ class Runner {
     rp.lcols[1] = lc[1];
     rp.status = status;
     reduce(rp, slot_base, c->G.d(), 0, (double)slot_base * per_slot * 8.0);
-    if (use_nccl && do_allreduce) {
-      Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
-      NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
-                               c->stream));
-    }
+    if (use_coll && do_allreduce) allreduce(c->G.d(), (size_t)M * p.N);
     if (count_sync) record(label, (long)M * p.N);
     return M;
   }
@@ -704,7 +797,7 @@ class Runner {
   }
   // launch (or hold back) the reduction of `slots` partial slots described by rp
   void reduce(const TileParams& rp, int slots, double* out, int ld_out, double bytes) {
-    if (defer_reduce && !use_nccl && !gout) {
+    if (defer_reduce && !use_coll && !gout) {
       pend.on = true;
       pend.a = reduce_args(rp, slots, out, ld_out);
       pend.entries = rp.mt_out * 8 * 8 * gram_n_tiles(rp.N);
@@ -773,11 +866,7 @@ class Runner {
         gout_ld = 0;
         row_off += len;
       }
-    if (use_nccl && do_allreduce) {
-      Prof pr(c, "nccl_allreduce", (double)M * N * 8.0, 0.0);
-      NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * N, ncclDouble, ncclSum, c->comm,
-                               c->stream));
-    }
+    if (use_coll && do_allreduce) allreduce(c->G.d(), (size_t)M * N);
     if (count_sync) record(label, (long)M * N);
     return M;
   }
@@ -887,11 +976,7 @@ class Runner {
     }
     p.partial = c->partial.d();
     reduce(p, cta_base, gout ? gout : c->G.d(), gout ? gout_ld : 0, (double)cta_base * per_cta * 8.0);
-    if (use_nccl && do_allreduce) {
-      Prof pr(c, "nccl_allreduce", (double)M * p.N * 8.0, 0.0);
-      NCCL_OK(nccl().AllReduce(c->G.p, c->G.p, (size_t)M * p.N, ncclDouble, ncclSum, c->comm,
-                               c->stream));
-    }
+    if (use_coll && do_allreduce) allreduce(c->G.d(), (size_t)M * p.N);
     if (count_sync) record(label, (long)M * p.N);
     return M;
   }
@@ -987,13 +1072,9 @@ class Runner {
                                    c->roots.d() + t * ss, status, c->stream, &c->launches));
     }
     const double* all_roots = c->roots.d();
-    if (use_nccl) {
-      NCCL_OK(nccl().GroupStart());
-      NCCL_OK(nccl().AllGather(c->roots.p, c->roots_all.p, ss, ncclDouble, c->comm, c->stream));
-      if (fusedG && fused_words > 0)
-        NCCL_OK(nccl().AllReduce(fusedG, fusedG, (size_t)fused_words, ncclDouble, ncclSum, c->comm,
-                                 c->stream));
-      NCCL_OK(nccl().GroupEnd());
+    if (use_coll) {
+      // one rendezvous: allgather of the per-rank roots + the fused Gram's allreduce
+      exchange(c->roots.d(), ss, c->roots_all.d(), fusedG, fusedG ? (size_t)fused_words : 0);
       all_roots = c->roots_all.d();
     }
     const double* mtop = nullptr;  // identity: a single shard's root is the global root
@@ -1004,7 +1085,7 @@ class Runner {
       Prof pr(c, "tsqr_tree", 0.0, 0.0);
       CUDA_OK(tsqr_cross_launch(all_roots, P, (int)s, c->cross_ws.d(), rout, ldrout,
                                 c->cross_m.d(), status, c->stream, &c->launches));
-      mtop = c->cross_m.d() + (use_nccl ? (size_t)c->rank * ss : 0);
+      mtop = c->cross_m.d() + (use_coll ? (size_t)c->rank * ss : 0);
     }
     for (size_t t = 0; t < sh.size(); ++t) {
       const Shard& x = sh[t];
@@ -1207,6 +1288,7 @@ class Runner {
         if (mode == OS_TSQR) tsqr(SQ, kp + si, kp + si, sdiag, si, "reduce_factor_tree:tsqr");
         M = gram(onesync_spec_unfused(mode, k + 1), lab);
       }
+      fire_probe(k, scol_nxt + kp, kp + si);  // S2 = rows kp.. of the next scol
       q_final(kp + si);  // later steps only write columns >= kp + s
       std::swap(scol_cur, scol_nxt);
     }
@@ -1438,7 +1520,10 @@ void validate(int variant, long n, long m, long s, int procs) {
   if (m > 4096) fail(BGS_E_CONFIG, "m = %ld exceeds the supported maximum 4096", m);
 }
 
-void select_device(bgs_ctx* c) { CUDA_OK(cudaSetDevice(c->device)); }
+void select_device(bgs_ctx* c) {
+  if (!c) fail(BGS_E_CUDA, "null context");
+  CUDA_OK(cudaSetDevice(c->device));
+}
 
 }  // namespace
 
@@ -1614,6 +1699,29 @@ int bgs_ctx_create(int device, int rank, int nranks, const void* uid, bgs_ctx** 
   }
 }
 
+int bgs_ctx_create_host_comm(int device, int rank, int nranks, bgs_allgather_fn fn, void* user,
+                             bgs_ctx** out, bgs_error* err) {
+  clear_err(err);
+  *out = nullptr;
+  if (!fn || nranks < 1 || rank < 0 || rank >= nranks) {
+    if (err) {
+      err->code = BGS_E_COLLECTIVE;
+      snprintf(err->msg, sizeof err->msg, "host communicator: need fn and 0 <= rank < nranks");
+    }
+    return BGS_E_COLLECTIVE;
+  }
+  bgs_ctx* c = nullptr;
+  // a plain single-GPU context, then the communicator
+  const int rc = bgs_ctx_create(device, 0, 1, nullptr, &c, err);
+  if (rc != BGS_OK) return rc;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->hc_fn = fn;
+  c->hc_user = user;
+  *out = c;
+  return BGS_OK;
+}
+
 int bgs_ctx_set_stream(bgs_ctx* c, void* stream) {
   if (!c) return BGS_E_CUDA;
   c->caller = static_cast<cudaStream_t>(stream);
@@ -1630,6 +1738,13 @@ void bgs_ctx_destroy(bgs_ctx* c) {
 int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const double* x,
                long ldx, double* q, long ldq, double* r, long ldr, bgs_stats* stats,
                bgs_timing* timing, bgs_error* err) {
+  return bgs_factor_opts(c, variant, n, m, s, procs, x, ldx, q, ldq, r, ldr, nullptr, stats,
+                         timing, err);
+}
+
+int bgs_factor_opts(bgs_ctx* c, int variant, long n, long m, long s, int procs, const double* x,
+                    long ldx, double* q, long ldq, double* r, long ldr, const bgs_options* opts,
+                    bgs_stats* stats, bgs_timing* timing, bgs_error* err) {
   clear_err(err);
   if (stats) memset(stats, 0, sizeof *stats);
   if (timing) memset(timing, 0, sizeof *timing);
@@ -1640,7 +1755,7 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
     if (ldx < n || ldq < n || ldr < m) fail(BGS_E_DIMENSION, "leading dimension too small");
     if (c->nranks > 1) fail(BGS_E_CONFIG, "bgs_factor runs on a single-GPU context; use bgs_factor_device per rank");
     select_device(c);
-    Runner run(c, variant, n, m, s, procs, false, stats);
+    Runner run(c, variant, n, m, s, procs, false, stats, opts);
     // Stream X in and Q out on copy engines, overlapped with the factorization, when both
     // host buffers are pinned (pageable copies would block the enqueueing thread).
     auto pinned = [](const void* p) {
@@ -1883,6 +1998,14 @@ int bgs_factor(bgs_ctx* c, int variant, long n, long m, long s, int procs, const
 int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0, long n_local,
                       const double* d_x, long ldx, double* d_q, long ldq, double* h_r, long ldr,
                       bgs_stats* stats, bgs_timing* timing, bgs_error* err) {
+  return bgs_factor_device_opts(c, variant, n, m, s, row0, n_local, d_x, ldx, d_q, ldq, h_r, ldr,
+                                nullptr, stats, timing, err);
+}
+
+int bgs_factor_device_opts(bgs_ctx* c, int variant, long n, long m, long s, long row0,
+                           long n_local, const double* d_x, long ldx, double* d_q, long ldq,
+                           double* h_r, long ldr, const bgs_options* opts, bgs_stats* stats,
+                           bgs_timing* timing, bgs_error* err) {
   clear_err(err);
   if (stats) memset(stats, 0, sizeof *stats);
   if (timing) memset(timing, 0, sizeof *timing);
@@ -1898,7 +2021,7 @@ int bgs_factor_device(bgs_ctx* c, int variant, long n, long m, long s, long row0
     if (ldx < n_local || ldq < n_local || ldr < m) fail(BGS_E_DIMENSION, "leading dimension too small");
     select_device(c);
     order_after_caller(c);
-    Runner run(c, variant, n, m, s, c->nranks, c->comm != nullptr, stats);
+    Runner run(c, variant, n, m, s, c->nranks, c->collective(), stats, opts);
     Shard sh;
     sh.row0 = row0;
     sh.rows = n_local;
@@ -1993,7 +2116,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
     (void)n;
     const int si = 8;
     // Q^T Q in panels of 8 right columns through K1 (+ NCCL allreduce)
-    Runner run(c, BGS_BCGSI_PLUS_P_1S, std::max(n, m), m, 1, c->nranks, c->comm != nullptr, nullptr);
+    Runner run(c, BGS_BCGSI_PLUS_P_1S, std::max(n, m), m, 1, c->nranks, c->collective(), nullptr);
     Shard sh;
     sh.rows = n_local;
     sh.X = d_x; sh.ldx = ldx;
@@ -2060,8 +2183,7 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
                               m, cudaMemcpyHostToDevice, c->stream));
     CUDA_OK(residual_launch(d_x, ldx, d_q, ldq, dr.d(), m, n_local, m, 1.0, 1.0, c->metrics.d(),
                             out2, c->sms, c->stream));
-    if (c->comm)
-      NCCL_OK(nccl().AllReduce(out2, out2, 2, ncclDouble, ncclSum, c->comm, c->stream));
+    if (c->collective()) run.allreduce(out2, 2);
     double h[2];
     CUDA_OK(cudaMemcpyAsync(h, out2, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
@@ -2163,6 +2285,7 @@ int bgs_gram(bgs_ctx* c, const double* a, long n, long ma, const double* b, long
     CUDA_OK(cudaMemcpyAsync(out, c->G.p, (size_t)ma * mb * sizeof(double), cudaMemcpyDeviceToHost,
                             c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
+    run.check_status();
     da.release();
     db.release();
     return BGS_OK;
@@ -2194,6 +2317,7 @@ int bgs_tsqr(bgs_ctx* c, const double* x, long n, long s, double* q, double* r, 
     run.tsqr(SX, 0, 0, c->rtop.d(), (int)s, "reduce_factor_tree:tsqr");
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaGetLastError());
+    run.check_status();  // rank-deficient leaves / non-finite input
     CUDA_OK(cudaMemcpy2D(q, n * sizeof(double), dq.p, ld * sizeof(double), n * sizeof(double), s,
                          cudaMemcpyDeviceToHost));
     CUDA_OK(cudaMemcpy(r, c->rtop.p, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToHost));

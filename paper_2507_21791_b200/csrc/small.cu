@@ -161,10 +161,15 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
   extern __shared__ double dyn[];
   const int s = p.s, kp = p.kp;
   const int tid = threadIdx.x;
-  // dynamic shared memory: [G gm x gn][scol_prev kp x s][scol_next (kp+s) x s]
+  // dynamic shared memory: [G gm x gn][scol_prev kp x s][scol_next (kp+s) x s], unless
+  // that exceeds the budget (p.unstaged: large m x s, e.g. s = 16 at m > 400): then every
+  // operand is read where it lies (global, L2-resident) with its own leading dimension
+  const bool stg = !p.unstaged;
   double* gs = dyn;
-  double* sprev = gs + (size_t)p.gm * p.gn;
-  double* snext = sprev + (size_t)kp * s;
+  double* sprev = stg ? gs + (size_t)p.gm * p.gn : nullptr;
+  double* snext = stg ? sprev + (size_t)kp * s : p.scol_next;
+  int ld_prev = kp;
+  const int ld_next = stg ? kp + s : p.ld_scol_next;
 
   // ---- stage every input with one parallel pass ----
   if (tid == 0) sh.flag = 0;
@@ -173,15 +178,25 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
     int bad = 0;
     for (int e = tid; e < p.gm * p.gn; e += kThreads) {
       const double v = p.G[(e % p.gm) + (size_t)(e / p.gm) * p.ldg];
-      gs[e] = v;
+      if (stg) gs[e] = v;
       bad |= !isfinite(v);
     }
     if (bad) atomicOr(&sh.flag, 1);
-    p.G = gs;  // every mode below reads the Gram from shared memory
-    p.ldg = p.gm;
+    if (stg) {
+      p.G = gs;  // every mode below reads the Gram from shared memory
+      p.ldg = p.gm;
+    }
   }
-  if (MODE == SM_ONESYNC_STEP) stage(p.scol_prev, p.ld_scol_prev, kp, s, sprev);
-  if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH) stage(p.aux1, p.ldaux1, kp, s, sprev);
+  if (stg) {
+    if (MODE == SM_ONESYNC_STEP) stage(p.scol_prev, p.ld_scol_prev, kp, s, sprev);
+    if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH) stage(p.aux1, p.ldaux1, kp, s, sprev);
+  } else if (MODE == SM_ONESYNC_STEP) {
+    sprev = const_cast<double*>(p.scol_prev);
+    ld_prev = p.ld_scol_prev;
+  } else if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH) {
+    sprev = const_cast<double*>(p.aux1);
+    ld_prev = p.ldaux1;
+  }
   for (int e = tid; e < s * s; e += kThreads) {
     if (p.sdiag) sh.sdp[e] = p.sdiag[e];
     if (MODE == SM_IRO_FINISH) {
@@ -259,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       if (sh.pivot) return;
       for (int e = tid; e < s * s; e += kThreads) p.ydiag[e] = sh.d[e];
       // R column = scol + Y S_diag; R_kk = Y_diag S_diag  (bcgs.cpp:332-333)
-      r_column(p, sprev, kp, Y, p.ldg, sh.sdp, s);
+      r_column(p, sprev, ld_prev, Y, p.ldg, sh.sdp, s);
       r_diag(p, sh.d, sh.sdp);
       if (!p.has_next) return;
       // S2 = Y_diag^{-T} (P - Y^T Z); scol = [Z; S2]  (bcgs.cpp:336-344)
@@ -282,13 +297,13 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       for (int e = tid; e < kn * s; e += kThreads) {
         const int i = e % kn, j = e / kn;
         const double v = i < kp ? Z[i + (size_t)j * p.ldg] : sh.c[(i - kp) + j * s];
-        snext[e] = v;
+        if (stg) snext[e] = v;
         p.scol_next[i + (size_t)j * p.ld_scol_next] = v;
       }
       if (p.os_mode == OS_PYTH) {
-        __syncthreads();
+        __syncthreads();  // (orders the global scol_next writes too: same block)
         // S_diag = chol(T - scol^T scol)  (bcgs.cpp:352-359)
-        cta_atb(snext, kn, snext, kn, kn, s, sh.a);
+        cta_atb(snext, ld_next, snext, ld_next, kn, s, sh.a);
         __syncthreads();
         if (tid < 32) {
           const double* T = p.G + kp + s + (size_t)s * p.ldg;
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       __syncthreads();
       if (sh.pivot) return;
       for (int e = tid; e < s * s; e += kThreads) p.ydiag[e] = sh.d[e];
-      r_column(p, sprev, kp, p.G, p.ldg, sh.sdp, s);
+      r_column(p, sprev, ld_prev, p.G, p.ldg, sh.sdp, s);
       r_diag(p, sh.d, sh.sdp);
       return;
     }
@@ -347,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
     }
     case SM_IRO_FINISH: {
       // R column = S1 + S2 R1; R_kk = R2 R1  (bcgs.cpp:162-164)
-      r_column(p, sprev, kp, p.G, p.ldg, sh.a, s);
+      r_column(p, sprev, ld_prev, p.G, p.ldg, sh.a, s);
       r_diag(p, sh.b, sh.a);
       return;
     }
@@ -718,16 +733,18 @@ cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches) {
     if (launches) *launches += 1;
     return cudaGetLastError();
   }
-  const size_t smem =
+  size_t smem =
       ((size_t)(p.gm > 0 ? p.gm * p.gn : 0) + (size_t)p.kp * p.s + (size_t)(p.kp + p.s) * p.s) *
       sizeof(double);
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  SmallParams q = p;
+  q.unstaged = smem > 200 * 1024 ? 1 : 0;  // read the operands from global memory instead
+  if (q.unstaged) smem = 0;
   cudaError_t e = cudaSuccess;
 #define BGS_SMALL_CASE(M)                      \
   case M:                                      \
     e = ensure_smem(small_kernel<M>, smem);    \
     if (e != cudaSuccess) return e;            \
-    small_kernel<M><<<1, kThreads, smem, st>>>(p); \
+    small_kernel<M><<<1, kThreads, smem, st>>>(q); \
     break;
   switch (p.mode) {
     BGS_SMALL_CASE(SM_ONESYNC_PROLOGUE)

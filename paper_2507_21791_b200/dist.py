@@ -7,7 +7,10 @@ NCCL unique id to every rank, gathers Q in rank order (gather_rows,
 communicator.cpp:319-336), checks the replicated factors bitwise across ranks
 (check_replication, runner.cpp:18-35) and takes max-over-ranks timings.  The per-step
 collective of the algorithm itself is the NCCL allreduce issued by the C library on its
-own stream (runtime.cu).
+own stream (runtime.cu) -- or, for ranks that share one GPU (NCCL refuses two ranks on a
+device), one ``host_allgather`` per sync through the library's host-communicator hook
+(bgs_ctx_create_host_comm): the partials travel over torch.distributed (gloo) and are
+summed in rank order by the library.
 """
 from __future__ import annotations
 
@@ -46,6 +49,20 @@ def exchange_unique_id(dist, rank: int, make_id: Callable[[], bytes]) -> bytes:
     if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
         raise RuntimeError("bad ncclUniqueId from rank 0")
     return bytes(uid)
+
+
+def host_allgather(dist) -> Callable[[bytes], bytes]:
+    """A blocking allgather of equal-size byte payloads over torch.distributed (the
+    ``host_allgather`` of api.Context): returns every rank's payload concatenated in rank
+    order (Communicator::rendezvous, communicator.cpp:96-144, over processes)."""
+    import torch
+
+    def allgather(payload: bytes) -> bytes:
+        t = torch.frombuffer(bytearray(payload), dtype=torch.uint8)
+        outs = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+        dist.all_gather(outs, t)
+        return b"".join(o.numpy().tobytes() for o in outs)
+    return allgather
 
 
 def gather_rows(dist, local: np.ndarray, n: int, world: int) -> np.ndarray:

@@ -60,3 +60,26 @@ def test_gpu_arm_contract():
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     v = d["verify"]
     assert v["sync_count"] == v["expected_syncs"] == 16 and v["loo"] < 1e-14
+
+
+def test_reference_arm_loads_nothing_of_the_product():
+    """The reference arm runs the reference's own code only: the product package is not
+    imported and libbgs_gpu.so is not mapped; ms_per_step is the measured sample time."""
+    code = (
+        "import sys, json, io, contextlib; sys.argv=['bench.py','--impl','reference','--steps','1',"
+        "'--warmup','0','--cpu-seconds','1']; import bench; buf=io.StringIO()\n"
+        "with contextlib.redirect_stdout(buf): bench.main()\n"
+        "maps=open('/proc/self/maps').read(); d=json.loads(buf.getvalue())\n"
+        "print(json.dumps({'pkg': any(m.startswith('paper_2507_21791_b200') for m in sys.modules),"
+        "'lib': 'libbgs_gpu' in maps, 'ref': 'libblockgs_ref' in maps or 'liboracle' in maps,"
+        "'line': d}))")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert not out["pkg"] and not out["lib"] and out["ref"]
+    d = out["line"]
+    rows = d["sample_rows"]
+    assert 400 <= rows <= 1_000_000 and str(rows) in d["cpu_baseline"]["sample"]
+    assert "note" not in d  # nothing extrapolated
+    assert d["steps"] == 1

@@ -66,3 +66,42 @@ def test_world2_rank_plumbing(n):
         assert ok_gather and ok_uid and ok_detect
         assert mx == 11.0
         assert shard == bgs.shard_rows(n, world, rank)
+
+
+def _ag_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2507_21791_b200 import dist as bd
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ag = bd.host_allgather(dist)
+        payload = np.arange(5, dtype=np.float64) + 100 * rank
+        out = np.frombuffer(ag(payload.tobytes()), dtype=np.float64).reshape(world, 5)
+        # the library sums the gathered partials in rank order: identical bits everywhere
+        tot = out[0].copy()
+        for r in range(1, world):
+            tot = tot + out[r]
+        q.put((rank, out.tolist(), tot.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_allgather_rank_order(world):
+    """dist.host_allgather (the host-communicator transport of bgs_ctx_create_host_comm):
+    every rank receives all payloads in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ag_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [[float(i + 100 * r) for i in range(5)] for r in range(world)]
+    for _, out, _ in res:
+        assert out == want
+    assert len({t for _, _, t in res}) == 1

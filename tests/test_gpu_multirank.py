@@ -1,0 +1,141 @@
+"""Multi-rank runs on the one GPU this pool lends: P processes share cuda:0, each with its
+own context, its own row shard and the library's host-communicator hook
+(bgs_ctx_create_host_comm) carried over torch.distributed gloo.  NCCL refuses two ranks on
+one device, and no kernel here waits on another rank (the exchange happens between
+launches), so this is safe on a single GPU (B200_PROFILING.md: no cross-rank spinning).
+
+What only runs with several real ranks is exercised: the per-step Gram allreduce, the
+prologue's TSQR root allgather fused with its Gram allreduce (one sync), the cross-rank
+TSQR tree with this rank's M offset, empty shards, and the reference's replication check
+(runner.cpp:18-35): R must be bitwise identical on every rank.  Results are compared with
+the oracle at the same procs (north_star tolerances) and the sync accounting is exact.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+U = 2.0 ** -53
+# (variant, n, m, s, procs, kappa, gaussian)
+CASES = [(v, 600, 32, 4, P, 1e3, False) for v in (1, 2, 3, 4, 5) for P in (2, 4)] + [
+    (3, 1000, 48, 4, 8, 1e2, True),
+    (5, 1000, 48, 4, 8, 1e2, True),
+    (4, 301, 24, 3, 3, 1e4, False),     # ragged split, s = 3
+    (3, 301, 24, 3, 3, 1e3, False),
+    (1, 130, 64, 8, 4, 1e5, False),     # s = 8: the unfused K2t / K1 path
+    (3, 12, 8, 4, 8, 1e1, True),        # ranks 6, 7 own no rows
+    (2, 12, 8, 2, 8, 1e1, True),
+    (3, 20000, 64, 4, 2, 1e6, False),   # the fused K12c path on each shard
+]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2507_21791_b200 as bgs
+    from oracle.oracle import Oracle
+    from paper_2507_21791_b200 import dist as bd
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = Oracle()
+        ctx = bgs.Context(0, rank, world, host_allgather=bd.host_allgather(dist))
+        for ci, (v, n, m, s, P, kappa, gauss) in enumerate(cases):
+            if P != world:
+                continue
+            x = o.gen_matrix(n, m, s, kappa, 4242 + ci, gauss)
+            r0, nl = bd.shard_range(n, world, rank)
+            ld = max(32, (nl + 31) // 32 * 32)
+            X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+            if nl:
+                X[:, :nl] = torch.from_numpy(np.ascontiguousarray(x[r0:r0 + nl].T)).cuda()
+            Q = torch.zeros_like(X)
+            try:
+                r, st, _ = bgs.factor_device(ctx, v, n, m, s, r0, nl, X.data_ptr(), ld,
+                                             Q.data_ptr(), ld)
+                bd.check_replication(dist, r)
+                qloc = Q[:, :nl].cpu().numpy().T.copy()
+                q.put((ci, rank, "ok", r, qloc, st.sync_count, st.words_reduced,
+                       list(st.event_labels)))
+            except Exception as e:  # noqa: BLE001
+                q.put((ci, rank, "err:" + str(e)[:300], None, None, 0, 0, []))
+        q.put((-1, rank, "done", None, None, 0, 0, []))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res, done = {}, 0
+    while done < world:
+        item = q.get(timeout=600)
+        if item[0] < 0:
+            done += 1
+            continue
+        res.setdefault(item[0], {})[item[1]] = item
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_ranks_sharing_one_gpu_match_oracle(oracle, world):
+    res = _run_world(world)
+    mine = [ci for ci, c in enumerate(CASES) if c[4] == world]
+    assert sorted(res) == mine
+    for ci in mine:
+        v, n, m, s, P, kappa, gauss = CASES[ci]
+        per = res[ci]
+        assert sorted(per) == list(range(world))
+        for rk in range(world):
+            assert per[rk][2] == "ok", (CASES[ci], per[rk][2])
+        x = oracle.gen_matrix(n, m, s, kappa, 4242 + ci, gauss)
+        ref = oracle.factor(v, x, s, P, metrics=True)
+        assert ref.rc == 0, ref.msg
+        r0 = per[0][3]
+        for rk in range(world):  # replicated R: bitwise identical on every rank
+            assert np.array_equal(per[rk][3].view(np.int64), r0.view(np.int64))
+            assert per[rk][5] == ref.sync_count and per[rk][6] == ref.words_reduced
+            assert per[rk][7] == ref.labels
+        q = np.vstack([per[rk][4] for rk in range(world)])
+        mx = np.abs(ref.r).max()
+        assert np.abs(r0 - ref.r).max() <= 1e-10 * mx, (CASES[ci], np.abs(r0 - ref.r).max() / mx)
+        assert np.all(np.tril(r0, -1) == 0.0) and np.all(np.diag(r0) >= 0.0)
+        loo, res_ = oracle.loo(q), oracle.residual(x, q, r0)
+        assert loo <= 10 * max(ref.loo, U), (CASES[ci], loo, ref.loo)
+        assert res_ <= 10 * max(ref.resid, U), (CASES[ci], res_, ref.resid)
+
+
+def test_multirank_matches_emulated_procs(oracle):
+    """The same factorization with 4 real ranks and with procs = 4 emulated on one
+    context: same sync accounting, R within rounding of each other."""
+    import paper_2507_21791_b200 as bgs
+    res = _run_world(4)
+    for ci, c in enumerate(CASES):
+        if c[4] != 4:
+            continue
+        v, n, m, s, P, kappa, gauss = c
+        x = oracle.gen_matrix(n, m, s, kappa, 4242 + ci, gauss)
+        emu = bgs.run_factor(v, x, s, P, metrics=False)
+        r = res[ci][0][3]
+        assert np.abs(r - emu.r).max() <= 1e-12 * np.abs(emu.r).max()
+        assert emu.stats.sync_count == res[ci][0][5]
