@@ -174,6 +174,13 @@ int bgs_gen_gaussian_device(bgs_ctx* ctx, unsigned long long seed, long row0, lo
 /* Host-side bitwise port of the reference generator's Gaussian mode
  * (matrix_gen.cpp:18-56: mt19937_64 + Box-Muller, column-major fill). */
 int bgs_gen_gaussian_host(unsigned long long seed, long n, long m, double* x, long ldx);
+/* Host-side bitwise port of gen_matrix (matrix_gen.cpp:18-97), both modes: gaussian != 0
+ * gives the raw N(0,1) draws, gaussian == 0 the geometric family X = U diag(sigma) V^T
+ * (Householder Q factors of seeded Gaussians, sigma_i = kappa^(-i/(m-1))).  Same checks
+ * and error wording as the reference (DimensionError / ConfigError).  O(n m^2) on one
+ * core: for driver-sized inputs (the bench configs), not for BASELINE config 5. */
+int bgs_gen_matrix_host(long n, long m, long s, double kappa, unsigned long long seed,
+                        int gaussian, double* x, long ldx, bgs_error* err);
 /* loss_of_orthogonality = ||Q^T Q - I||_2 and residual ||X - QR||_F / ||X||_F
  * computed on the GPU for a (sharded) device-resident factorization; the Gram and the
  * residual sum are reduced over ranks with NCCL. */

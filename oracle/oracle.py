@@ -146,6 +146,8 @@ class Reference:
         lib.ref_variant_flops.restype = D
         lib.ref_expected_syncs.argtypes = [I, L]
         lib.ref_expected_syncs.restype = L
+        lib.ref_set_classic_intra.argtypes = [I]
+        lib.ref_set_classic_intra.restype = None
 
     @staticmethod
     def available(path: str = REF_SO) -> bool:
@@ -160,7 +162,8 @@ class Reference:
             raise ValueError(msg.value.decode())
         return x
 
-    def factor(self, v, x, s, procs=1, metrics=False, want_q=True) -> Result:
+    def factor(self, v, x, s, procs=1, metrics=False, want_q=True, classic_intra=0) -> Result:
+        self.lib.ref_set_classic_intra(int(classic_intra))
         x = _f(x)
         n, m = x.shape
         q = np.zeros((n, m), order="F") if want_q else None

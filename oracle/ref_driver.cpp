@@ -66,6 +66,10 @@ int ref_gen_matrix(long n, long m, long s, double kappa, unsigned long long seed
 // success, an error code otherwise (NotSpd: 2, pivot in *pivot).  Timing covers
 // distribute + run_variant only (stats and gather excluded), as SURVEY.md §8(d).
 // labels: '\n'-joined event labels (factorization phase).  Metrics optional.
+// BcgsOptions::classic_intra for the following ref_factor calls (0 Tsqr, 1 CholQr).
+static int g_classic_intra = 0;
+void ref_set_classic_intra(int kind) { g_classic_intra = kind; }
+
 int ref_factor(int variant, const double* xin, long n, long m, long s, int procs,
                int want_metrics, double* q, double* r, long* sync_count, long* words,
                char* labels, long labcap, double* loo, double* resid, double* seconds,
@@ -78,7 +82,9 @@ int ref_factor(int variant, const double* xin, long n, long m, long s, int procs
     auto [views, st] = run_spmd(procs, [&](Communicator& comm) {
       auto t0 = std::chrono::steady_clock::now();
       DistBlockMatrix xd = distribute(x, s, comm);
-      BcgsResult res = run_variant(v, xd, comm, {});
+      BcgsOptions opts;
+      opts.classic_intra = g_classic_intra ? IntraorthKind::CholQr : IntraorthKind::Tsqr;
+      BcgsResult res = run_variant(v, xd, comm, opts);
       double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       DenseMatrix qf = gather(res.q);
       return View{std::move(qf), std::move(res.r), std::move(res.stats), secs};

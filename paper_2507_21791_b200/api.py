@@ -160,6 +160,7 @@ def _load() -> ctypes.CDLL:
         "bgs_profile_read": ([P, P, I, P], I),
         "bgs_tsqr": ([P, P, L, L, P, P, P], I),
         "bgs_ctx_create_host_comm": ([I, I, I, P, P, P, P], I),
+        "bgs_gen_matrix_host": ([L, L, L, D, ctypes.c_ulonglong, I, P, L, P], I),
         "bgs_factor_opts": ([P, I, L, L, L, I, P, L, P, L, P, L, P, P, P, P], I),
         "bgs_factor_device_opts": ([P, I, L, L, L, L, L, P, L, P, L, P, L, P, P, P, P], I),
     }
@@ -179,7 +180,7 @@ EXPORTED_SYMBOLS = (
     "bgs_device_info", "bgs_factor", "bgs_factor_device", "bgs_gen_gaussian_device",
     "bgs_gen_gaussian_host", "bgs_metrics", "bgs_metrics_device", "bgs_gram", "bgs_tsqr",
     "bgs_profile_enable", "bgs_profile_read", "bgs_ctx_create_host_comm", "bgs_factor_opts",
-    "bgs_factor_device_opts",
+    "bgs_factor_device_opts", "bgs_gen_matrix_host",
 )
 
 # bgs_allgather_fn / bgs_probe_fn (include/bgs_gpu.h)
@@ -211,7 +212,7 @@ def _raise(rc: int, err: _Err) -> None:
 
 
 class VariantId(enum.IntEnum):
-    Bcgs = 0  # classic BCGS (out of scope for the GPU path)
+    Bcgs = 0  # classic BCGS (classic_impl; BcgsOptions.classic_intra picks TSQR / CholQR)
     BcgsIro = 1  # BCGSI+
     BcgsPipiPlus = 2  # BCGSPIPI+
     BcgsIp1s = 3  # BCGSI+P-1S
@@ -529,6 +530,18 @@ def tsqr(x: np.ndarray, *, ctx: Optional[Context] = None) -> tuple[np.ndarray, n
     rc = _lib.bgs_tsqr(ctx.handle, _ptr(xf), n, s, _ptr(q), _ptr(r), ctypes.byref(err))
     _raise(rc, err)
     return q, r
+
+
+def gen_matrix(n: int, m: int, s: int = 1, kappa: float = 1.0, seed: int = 0,
+               gaussian: bool = False) -> np.ndarray:
+    """gen_matrix (matrix_gen.hpp:27, matrix_gen.cpp:18-97), bit for bit: the geometric
+    family (default, like MatrixSpec) or the raw Gaussian draws.  Host, one core."""
+    x = np.zeros((n, m), dtype=np.float64, order="F")
+    err = _Err()
+    _raise(_lib.bgs_gen_matrix_host(int(n), int(m), int(s), float(kappa), int(seed),
+                                    1 if gaussian else 0, _ptr(x) if x.size else None,
+                                    max(int(n), 1), ctypes.byref(err)), err)
+    return x
 
 
 def gen_gaussian_host(seed: int, n: int, m: int) -> np.ndarray:

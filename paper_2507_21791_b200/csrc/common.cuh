@@ -30,6 +30,7 @@ enum Site : int {
   SITE_PROLOGUE_PYTH = 1,   // "prologue Pythagorean normalization"
   SITE_FIRST_PASS = 2,      // "first-pass Pythagorean normalization"
   SITE_SECOND_PASS = 3,     // "second-pass Pythagorean normalization"
+  SITE_INTRA_CHOLQR = 4,    // "intra-block Cholesky QR" (classic BCGS, bcgs.cpp:111, 123)
 };
 struct DevStatus {
   int code;

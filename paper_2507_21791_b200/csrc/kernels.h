@@ -122,6 +122,7 @@ struct UpdateParams {
   const DevStatus* status;
 };
 cudaError_t update_launch(const UpdateParams& p, int num_sms, cudaStream_t st, int* launches);
+int update_max_kp(int s);
 
 // ---------------- K3: replicated small factor ops (small.cu) ----------------
 enum SmallMode : int {
@@ -132,6 +133,8 @@ enum SmallMode : int {
   SM_IRO_SAVE = 5,          // keep S1 = Q^T X_k (bcgs.cpp:151-153)
   SM_IRO_FINISH = 6,        // R column = S1 + S2 R1, R_kk = R2 R1 (bcgs.cpp:162-164)
   SM_COPY_RBLOCK = 7,       // R(0,0) = TSQR root (bcgs.cpp:83-90, 142-146)
+  SM_CLASSIC_FINISH = 8,    // R column = S (saved), R_kk = intra-block R (bcgs.cpp:126-128)
+  SM_CHOLQR = 9,            // R_kk = chol(U^T U) -> sdiag (cholqr, intraorth.cpp:136-151)
 };
 // onesync sub-modes (SDiagMode, bcgs.cpp:223-231)
 enum OnesyncMode : int { OS_PYTH = 0, OS_SKIP = 1, OS_TSQR = 2 };

@@ -1024,7 +1024,38 @@ class Runner {
       const int nout = (u.has_a ? 1 : 0) + (u.has_b ? 1 : 0);
       Prof pr(c, "update", 8.0 * x.rows * ((double)u.kp + 2.0 * s * nout),
               2.0 * x.rows * (double)u.kp * s * nout + (double)x.rows * s * s * nout);
-      CUDA_OK(update_launch(p, c->sms, c->stream, &c->launches));
+      // A prefix longer than one launch's coefficient panel (s = 16 past m ~ 880): chained
+      // launches over column chunks, in place; the triangular factors and B's coupling to A
+      // act in the last one.
+      static const int kmax_env = [] {
+        const char* e = getenv("BGS_UPDATE_MAXKP");  // tests: force the chained path
+        return e ? atoi(e) : 0;
+      }();
+      int kmax = update_max_kp((int)s);
+      if (kmax_env > 0) kmax = std::min(kmax, std::max(4, kmax_env & ~3));
+      if (u.kp <= kmax) {
+        CUDA_OK(update_launch(p, c->sms, c->stream, &c->launches));
+        continue;
+      }
+      for (int c0 = 0; c0 < u.kp; c0 += kmax) {
+        const int c1 = std::min(u.kp, c0 + kmax);
+        const bool last = c1 == u.kp;
+        UpdateParams pc = p;
+        pc.kp = c1 - c0;
+        pc.qp = x.Q + (size_t)c0 * x.ldq;
+        if (u.has_a) {
+          pc.CA = u.CA + c0;
+          pc.TA = last ? u.TA : nullptr;
+          if (c0 > 0) { pc.srcA = pc.dstA; pc.ld_srcA = pc.ld_dstA; }
+        }
+        if (u.has_b) {
+          pc.CB = u.CB + c0;
+          pc.TB = last ? u.TB : nullptr;
+          pc.cb_has_a = last ? u.cb_has_a : 0;
+          if (c0 > 0) { pc.srcB = pc.dstB; pc.ld_srcB = pc.ld_dstB; }
+        }
+        CUDA_OK(update_launch(pc, c->sms, c->stream, &c->launches));
+      }
     }
   }
 
@@ -1294,6 +1325,69 @@ class Runner {
     }
   }
 
+  // classic_impl (bcgs.cpp:92-133): one projection, then the intra-block QR (TSQR, or
+  // Cholesky QR when BcgsOptions::classic_intra says so) of X_k - Q_{1:k} S.
+  void intra_qr(int src, long col, long k) {
+    const int si = (int)s;
+    const bool chol = opt && opt->classic_intra == 1;
+    if (!chol) {
+      tsqr(src, col, col, c->r1.d(), si, "reduce_factor_tree:tsqr");
+      return;
+    }
+    // cholqr (intraorth.cpp:136-151): G = U^T U (one sync), R = chol(G), Q = U R^{-1}
+    GramSpec g = spec1(src, (int)col, si, si);
+    add_right(g, 0, 0, si);
+    const int M = gram(g, "fused_gram:cholqr");
+    SmallParams sp;
+    memset(&sp, 0, sizeof sp);
+    sp.mode = SM_CHOLQR;
+    sp.k = (int)k;
+    sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+    sp.sdiag = c->r1.d();
+    small(sp);
+    Upd u;
+    u.kp = 0;
+    u.has_a = true;
+    u.srcA = src; u.colA = col; u.dstA = col;
+    u.TA = c->r1.d();
+    update(u);
+  }
+  void classic() {
+    if (q == 1) return single_block();
+    const int si = (int)s;
+    SmallParams sp;
+    memset(&sp, 0, sizeof sp);
+    intra_qr(SX, 0, 0);
+    sp.mode = SM_CLASSIC_FINISH;  // R(0,0)
+    sp.rtop = c->r1.d(); sp.ldrtop = si;
+    small(sp);
+    for (long k = 1; k < q; ++k) {
+      const int kp = (int)(k * s);
+      GramSpec g = spec2(SQ, 0, kp, kp, SX, kp, si, 0);
+      add_right(g, 1, 0, si);
+      const int M = gram(g, "fused_gram:proj");
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_IRO_SAVE;
+      sp.k = (int)k; sp.kp = kp;
+      sp.G = c->G.d(); sp.ldg = M; sp.gm = M; sp.gn = si;
+      sp.save = c->save.d(); sp.ldsave = kp;
+      small(sp);
+      Upd u;
+      u.kp = kp;
+      u.has_a = true;
+      u.srcA = SX; u.colA = kp; u.dstA = kp;
+      u.CA = c->save.d(); u.ldca = kp; u.TA = nullptr;
+      update(u);
+      intra_qr(SQ, kp, k);
+      memset(&sp, 0, sizeof sp);
+      sp.mode = SM_CLASSIC_FINISH;
+      sp.k = (int)k; sp.kp = kp;
+      sp.aux1 = c->save.d(); sp.ldaux1 = kp;
+      sp.rtop = c->r1.d(); sp.ldrtop = si;
+      small(sp);
+    }
+  }
+
   // pipi_impl (bcgs.cpp:169-219)
   void pipi() {
     if (q == 1) return single_block();
@@ -1460,6 +1554,7 @@ class Runner {
     }
     setup();
     switch (variant) {
+      case BGS_BCGS: classic(); break;
       case BGS_BCGSI_PLUS: iro(); break;
       case BGS_BCGSPIPI_PLUS: pipi(); break;
       case BGS_BCGSI_PLUS_P_1S: onesync(OS_PYTH, 2); break;
@@ -1483,6 +1578,7 @@ class Runner {
     if (h.code == ST_NOT_SPD) {
       const char* site = h.site == SITE_PROLOGUE_PYTH ? "prologue Pythagorean normalization"
                          : h.site == SITE_FIRST_PASS  ? "first-pass Pythagorean normalization"
+                         : h.site == SITE_INTRA_CHOLQR ? "intra-block Cholesky QR"
                                                       : "second-pass Pythagorean normalization";
       f.site = site;
       std::string hyp;
@@ -1515,7 +1611,6 @@ void validate(int variant, long n, long m, long s, int procs) {
   if (n < m)
     fail(BGS_E_DIMENSION, "bcgs: economic factorization needs at least as many rows as columns");
   if (variant < 0 || variant > 5) fail(BGS_E_CONFIG, "unknown variant id %d", variant);
-  if (variant == BGS_BCGS) fail(BGS_E_CONFIG, "BCGS (classic) is out of scope for the GPU path");
   if (s > 16) fail(BGS_E_CONFIG, "block width s = %ld exceeds the supported maximum 16", s);
   if (m > 4096) fail(BGS_E_CONFIG, "m = %ld exceeds the supported maximum 4096", m);
 }

@@ -189,11 +189,12 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
   }
   if (stg) {
     if (MODE == SM_ONESYNC_STEP) stage(p.scol_prev, p.ld_scol_prev, kp, s, sprev);
-    if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH) stage(p.aux1, p.ldaux1, kp, s, sprev);
+      if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH || MODE == SM_CLASSIC_FINISH)
+      stage(p.aux1, p.ldaux1, kp, s, sprev);
   } else if (MODE == SM_ONESYNC_STEP) {
     sprev = const_cast<double*>(p.scol_prev);
     ld_prev = p.ld_scol_prev;
-  } else if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH) {
+  } else if (MODE == SM_PIPI_REPROJ || MODE == SM_IRO_FINISH || MODE == SM_CLASSIC_FINISH) {
     sprev = const_cast<double*>(p.aux1);
     ld_prev = p.ldaux1;
   }
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       sh.a[e] = p.aux2[(e % s) + (size_t)(e / s) * p.ldaux2];  // R1
       sh.b[e] = p.rtop[(e % s) + (size_t)(e / s) * p.ldrtop];  // R2
     }
-    if (MODE == SM_ONESYNC_PROLOGUE || MODE == SM_COPY_RBLOCK)
+    if (MODE == SM_ONESYNC_PROLOGUE || MODE == SM_COPY_RBLOCK || MODE == SM_CLASSIC_FINISH)
       sh.b[e] = p.rtop[(e % s) + (size_t)(e / s) * p.ldrtop];  // root R
   }
   __syncthreads();
@@ -364,6 +365,30 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
       // R column = S1 + S2 R1; R_kk = R2 R1  (bcgs.cpp:162-164)
       r_column(p, sprev, ld_prev, p.G, p.ldg, sh.a, s);
       r_diag(p, sh.b, sh.a);
+      return;
+    }
+    case SM_CLASSIC_FINISH: {
+      // store_column_blocks(R, k, S); R.set_block(k, k, R_intra)  (bcgs.cpp:126-128)
+      for (int e = tid; e < kp * s; e += kThreads) {
+        const int i = e % kp, j = e / kp;
+        p.R[i + (size_t)(kp + j) * p.ldr] = sprev[i + (size_t)j * ld_prev];
+      }
+      for (int e = tid; e < s * s; e += kThreads) {
+        const int i = e % s, j = e / s;
+        p.R[(kp + i) + (size_t)(kp + j) * p.ldr] = i <= j ? sh.b[e] : 0.0;
+      }
+      return;
+    }
+    case SM_CHOLQR: {
+      // R = chol_factor(U^T U) (intraorth.cpp:146-149); NotSpd -> "intra-block Cholesky QR"
+      if (tid < 32) {
+        for (int e = tid; e < s * s; e += 32) sh.c[e] = p.G[(e % s) + (size_t)(e / s) * p.ldg];
+        __syncwarp();
+        const int piv = chol_warp(sh.c, s, sh.d);
+        if (piv && tid == 0) set_status(p.status, ST_NOT_SPD, piv, p.k + 1, SITE_INTRA_CHOLQR, 2);
+        __syncwarp();
+        for (int e = tid; e < s * s; e += 32) p.sdiag[e] = sh.d[e];
+      }
       return;
     }
     default:
@@ -754,6 +779,8 @@ cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches) {
     BGS_SMALL_CASE(SM_IRO_SAVE)
     BGS_SMALL_CASE(SM_IRO_FINISH)
     BGS_SMALL_CASE(SM_COPY_RBLOCK)
+    BGS_SMALL_CASE(SM_CLASSIC_FINISH)
+    BGS_SMALL_CASE(SM_CHOLQR)
     default: return cudaErrorInvalidValue;
   }
 #undef BGS_SMALL_CASE

@@ -350,6 +350,20 @@ static cudaError_t launch_s(const UpdateParams& p, int grid, size_t smem, cudaSt
   return cudaGetLastError();
 }
 
+// Longest prefix one launch can take (the coefficient panel lives in shared memory); the
+// runtime splits longer prefixes into chained launches (Runner::update).
+int update_max_kp(int s) {
+  const int S = s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : s <= 8 ? 8 : 16;
+  int best = 0;
+  for (int kp = 4; kp <= 8192; kp += 4) {
+    const bool tc = S >= 8 && (S == 8 ? tc_smem<8>(kp) : tc_smem<16>(kp)) <= 220 * 1024;
+    const bool sc = ((size_t)kp * 2 * S + 3 * S * S) * sizeof(double) + 16 <= 200 * 1024;
+    if (tc || sc) best = kp;
+    else break;
+  }
+  return best;
+}
+
 cudaError_t update_launch(const UpdateParams& p, int num_sms, cudaStream_t st, int* launches) {
   const int s = p.s;
   const int S = s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : s <= 8 ? 8 : 16;

@@ -324,7 +324,7 @@ def test_malformed_inputs_rejected(gpu_ctx):
     with pytest.raises(bgs.api.DimensionError):
         bgs.run_factor(1, np.ones((4, 8)), 2, 1)
     with pytest.raises(bgs.api.ConfigError):
-        bgs.run_factor(0, np.ones((40, 8)), 2, 1)
+        bgs.run_factor(6, np.ones((40, 8)), 2, 1)  # unknown variant id
 
 
 def test_variants_agree_on_benign_input(oracle, gpu_ctx):
@@ -856,3 +856,54 @@ def test_m2048_properties(gpu_ctx, v):
     assert out.stats.sync_count == bgs.expected_syncs(v, 512)
     assert_structure(out.r)
     assert out.loo <= 1e-13 and out.resid <= 1e-14, (out.loo, out.resid)
+
+
+# ---------------------------------------------------------------------------------------
+# Classic BCGS (classic_impl, bcgs.cpp:92-133) with both intra-block kernels
+# (BcgsOptions::classic_intra: TSQR, or Cholesky QR), against the compiled reference
+# itself (oracle/_ref; the C restatement does not carry classic BCGS).
+# ---------------------------------------------------------------------------------------
+def _reference():
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    return Reference()
+
+
+@pytest.mark.parametrize("intra", [0, 1], ids=["tsqr", "cholqr"])
+@pytest.mark.parametrize("n,m,s,procs,kappa", [(1000, 32, 4, 1, 1e2), (777, 36, 3, 3, 1e3),
+                                               (2000, 64, 8, 2, 1e2), (300, 48, 16, 1, 1e1),
+                                               (64, 8, 2, 1, 1e2)])
+def test_classic_bcgs_matches_reference(gpu_ctx, intra, n, m, s, procs, kappa):
+    import paper_2507_21791_b200 as bgs
+    ref_lib = _reference()
+    x = ref_lib.gen_matrix(n, m, s, kappa, 99, False)
+    ref = ref_lib.factor(0, x, s, procs, metrics=True, classic_intra=intra)
+    assert ref.rc == 0, ref.msg
+    out = bgs.run_factor(0, x, s, procs, metrics=False, ctx=gpu_ctx,
+                         opts=bgs.BcgsOptions(classic_intra=intra))
+    assert out.ok, out.error
+    assert out.stats.sync_count == ref.sync_count == bgs.expected_syncs(0, m // s)
+    assert out.stats.event_labels == ref.labels
+    assert out.stats.words_reduced == ref.words_reduced
+    assert_r_close(out.r, ref.r)
+    assert_structure(out.r)
+    from oracle.oracle import Oracle
+    o = Oracle()
+    loo, res = o.loo(out.q), o.residual(x, out.q, out.r)
+    assert loo <= 10 * max(ref.loo, U) and res <= 10 * max(ref.resid, U), (loo, ref.loo)
+
+
+def test_classic_cholqr_not_spd_diagnostic(gpu_ctx):
+    """Cholesky QR of a numerically rank-deficient block: NotSpd with the reference's
+    site wording (bcgs.cpp:111-113, 122-124) and assumption power 2."""
+    import paper_2507_21791_b200 as bgs
+    ref_lib = _reference()
+    x = ref_lib.gen_matrix(400, 32, 4, 1.0, 5, True)
+    x[:, 2] = 0.0  # the first block's Gram is singular: pivot 3 is exactly 0
+    ref = ref_lib.factor(0, x, 4, 1, metrics=False, classic_intra=1)
+    out = bgs.run_factor(0, x, 4, 1, metrics=False, ctx=gpu_ctx,
+                         opts=bgs.BcgsOptions(classic_intra=1))
+    assert ref.rc == 2 and not out.ok
+    assert out.error == ref.msg, (out.error, ref.msg)
+    assert out.not_spd_pivot == ref.pivot == 3
