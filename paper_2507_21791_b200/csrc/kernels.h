@@ -124,6 +124,25 @@ struct UpdateParams {
 cudaError_t update_launch(const UpdateParams& p, int num_sms, cudaStream_t st, int* launches);
 int update_max_kp(int s);
 
+// ---------------- K2m: the s = 8 / 16 update fed by TMA (update_tma.cu) ----------------
+struct alignas(64) UpdTmaParams {
+  CUtensorMap map[5];  // the Q buffer, 3-D boxes {16, 4, w}, w = 128/64/32/16/8
+  int col0;            // first prefix column in the map
+  long n_rows;
+  long total_blocks;   // 32-row blocks (set by the launcher)
+  int kp, s;           // kp: multiple of 8
+  int stages;          // ring depth (set by the launcher)
+  int has_a, has_b, cb_has_a;
+  const double* srcA; long ld_srcA; double* dstA; long ld_dstA;
+  const double* CA; long ldca; const double* TA;
+  const double* srcB; long ld_srcB; double* dstB; long ld_dstB;
+  const double* CB; long ldcb; const double* TB;
+  const DevStatus* status;
+};
+cudaError_t update_tma_launch(UpdTmaParams& p, int num_sms, cudaStream_t st, int* launches);
+int update_tma_max_kp(int s);
+size_t update_tma_smem_bytes(int s, int kp, int stages);
+
 // ---------------- K3: replicated small factor ops (small.cu) ----------------
 enum SmallMode : int {
   SM_ONESYNC_PROLOGUE = 1,  // scol = R00^{-T} G0[0:s]; Sd = pyth ? chol(T - scol^T scol) : I

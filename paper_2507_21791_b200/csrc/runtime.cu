@@ -433,6 +433,7 @@ class Runner {
   bool no_merge_small = false;  // BGS_NO_MERGE_SMALL: separate reduce and small launches
   bool no_pdl = false;          // BGS_NO_PDL: no programmatic dependent launch of K12c
   int comp_mode = 1;            // BGS_COMP_TAIL: 0 off, 1 BCGSI+1S (default), 2 all modes
+  bool no_k2m = false;          // BGS_K2M=0: the s = 8 / 16 update on K2t instead of K2m
   // Programmatic dependent launch of a fused kernel is allowed only right behind the
   // merged reduce + step kernel (nothing queued in between): that kernel writes only the
   // Gram, the small factors and the status word, which the fused kernel reads after its
@@ -457,6 +458,8 @@ class Runner {
     gram_max_units = e4 ? atoi(e4) : 0;
     const char* e5 = getenv("BGS_NO_MERGE_SMALL");
     no_merge_small = e5 && *e5 && *e5 != '0';
+    const char* ek2m = getenv("BGS_K2M");
+    no_k2m = ek2m && *ek2m == '0';
     const char* ect = getenv("BGS_COMP_TAIL");
     comp_mode = !ect ? 1 : (*ect == '0' ? 0 : (strcmp(ect, "all") == 0 ? 2 : 1));
     const char* e6 = getenv("BGS_NO_PDL");
@@ -1031,6 +1034,38 @@ class Runner {
         const char* e = getenv("BGS_UPDATE_MAXKP");  // tests: force the chained path
         return e ? atoi(e) : 0;
       }();
+      // s = 5..16 with kp a multiple of 8: K2m (update_tma.cu), TMA-fed; BGS_K2M=0: K2t
+      if (!no_k2m && s >= 5 && s <= 16 && u.kp >= 8 && u.kp % 8 == 0) {
+        int km = update_tma_max_kp((int)s) & ~7;
+        if (kmax_env > 0) km = std::min(km, std::max(8, kmax_env & ~7));
+        for (int c0 = 0; c0 < u.kp; c0 += km) {
+          const int c1 = std::min(u.kp, c0 + km);
+          const bool last = c1 == u.kp;
+          UpdTmaParams q;
+          memset(&q, 0, sizeof q);
+          for (int wi = 0; wi < 5; ++wi) q.map[wi] = x.mapQ[1][wi];  // boxes {16, 4, w}
+          q.col0 = c0;
+          q.n_rows = x.rows;
+          q.kp = c1 - c0;
+          q.s = (int)s;
+          q.has_a = u.has_a;
+          q.has_b = u.has_b;
+          q.cb_has_a = last ? u.cb_has_a : 0;
+          q.status = status;
+          if (u.has_a) {
+            q.srcA = c0 > 0 ? p.dstA : p.srcA; q.ld_srcA = c0 > 0 ? p.ld_dstA : p.ld_srcA;
+            q.dstA = p.dstA; q.ld_dstA = p.ld_dstA;
+            q.CA = u.CA + c0; q.ldca = u.ldca; q.TA = last ? u.TA : nullptr;
+          }
+          if (u.has_b) {
+            q.srcB = c0 > 0 ? p.dstB : p.srcB; q.ld_srcB = c0 > 0 ? p.ld_dstB : p.ld_srcB;
+            q.dstB = p.dstB; q.ld_dstB = p.ld_dstB;
+            q.CB = u.CB + c0; q.ldcb = u.ldcb; q.TB = last ? u.TB : nullptr;
+          }
+          CUDA_OK(update_tma_launch(q, c->sms, c->stream, &c->launches));
+        }
+        continue;
+      }
       int kmax = update_max_kp((int)s);
       if (kmax_env > 0) kmax = std::min(kmax, std::max(4, kmax_env & ~3));
       if (u.kp <= kmax) {

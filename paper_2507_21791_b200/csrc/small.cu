@@ -151,7 +151,22 @@ __device__ __noinline__ void r_diag(const SmallParams& p, const double* a, const
 // Copies an r x c column-major global block into shared memory (ld = r) with one
 // coalesced pass: all loads of a thread are independent, so the L2 latency is paid once.
 __device__ __noinline__ void stage(const double* src, int ld, int r, int c, double* dst) {
-  for (int e = threadIdx.x; e < r * c; e += kThreads) dst[e] = src[(e % r) + (size_t)(e / r) * ld];
+  // batches of 8 independent loads per thread before their stores (L2 latency once per
+  // batch, not per element)
+  const int tot = r * c;
+  for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * kThreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kThreads;
+      v[u] = e < tot ? src[(e % r) + (size_t)(e / r) * ld] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e < tot) dst[e] = v[u];
+    }
+  }
 }
 
 template <int MODE>
@@ -176,10 +191,22 @@ __global__ void __launch_bounds__(kThreads, 1) small_kernel(SmallParams p) {
   __syncthreads();
   if (p.gm > 0) {
     int bad = 0;
-    for (int e = tid; e < p.gm * p.gn; e += kThreads) {
-      const double v = p.G[(e % p.gm) + (size_t)(e / p.gm) * p.ldg];
-      if (stg) gs[e] = v;
-      bad |= !isfinite(v);
+    const int tot = p.gm * p.gn;
+    for (int e0 = tid; e0 < tot; e0 += 8 * kThreads) {  // 8 loads in flight per thread
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kThreads;
+        v[u] = e < tot ? p.G[(e % p.gm) + (size_t)(e / p.gm) * p.ldg] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e < tot) {
+          if (stg) gs[e] = v[u];
+          bad |= !isfinite(v[u]);
+        }
+      }
     }
     if (bad) atomicOr(&sh.flag, 1);
     if (stg) {

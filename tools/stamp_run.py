@@ -5,7 +5,8 @@ sys.path.insert(0, ".")
 import paper_2507_21791_b200 as bgs
 from paper_2507_21791_b200 import api
 lib = api._lib
-n, m, s = 1_000_000, 400, 4
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+m, s = 400, 4
 ld = (n + 31) // 32 * 32
 ctx = bgs.Context(0)
 X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
@@ -33,3 +34,8 @@ for k in range(1, m // s - 1):
               f"CTA ends spread {x1-x0:6d} of kernel {x1-e0:7d}")
 print("mean step", np.mean(dur), "mean first entry", np.mean(gaps), "mean last ready", np.mean(rdy),
       "mean CTA-end spread", np.mean(spread), "sum spread ms", np.sum(spread) / 1e6)
+# per-phase means of the reduce + step kernel: [start, reduce done, detect, pass, products,
+# chol, trsm, end] (small.cu STAMP points)
+ph = np.diff(st[1:m // s - 1, :8], axis=1).mean(axis=0)
+print("phases (ns): reduce %.0f detect %.0f pass %.0f products %.0f chol1 %.0f trsm %.0f chol2+stores %.0f"
+      % tuple(ph))
