@@ -550,7 +550,7 @@ class Runner {
     c->status.ensure(sizeof(DevStatus));
     status = reinterpret_cast<DevStatus*>(c->status.p);
     CUDA_OK(cudaMemsetAsync(status, 0, sizeof(DevStatus), c->stream));
-    c->ticket.ensure(64);
+    c->ticket.ensure(kTicketBytes);
     CUDA_OK(cudaMemsetAsync(c->ticket.p, 0, 64, c->stream));
     c->R.ensure((size_t)m * m * sizeof(double));
     CUDA_OK(cudaMemsetAsync(c->R.p, 0, (size_t)m * m * sizeof(double), c->stream));

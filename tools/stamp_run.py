@@ -39,3 +39,14 @@ print("mean step", np.mean(dur), "mean first entry", np.mean(gaps), "mean last r
 ph = np.diff(st[1:m // s - 1, :8], axis=1).mean(axis=0)
 print("phases (ns): reduce %.0f detect %.0f pass %.0f products %.0f chol1 %.0f trsm %.0f chol2+stores %.0f"
       % tuple(ph))
+# raw timeline around a few steps (ns, relative to the step kernel's start of step k):
+# fused kernel of kp = k s (entry min / ready max / CTA end min, max) and step kernel k
+for k in (10, 50, 90):
+    if k >= m // s - 1:
+        continue
+    t0 = st[k, 0]
+    e0, e1, w0, w1, x0, x1, r0, r1 = kt[k]
+    print(f"k {k}: fused(kp={k * s}) entry {e0 - t0} ready {r1 - t0} end {x0 - t0}..{x1 - t0} | "
+          f"step {k}: start 0 reduced {st[k, 1] - t0} end {st[k, 7] - t0} | "
+          f"fused(kp={(k + 1) * s}) entry {kt[k + 1, 0] - t0} ready {kt[k + 1, 7] - t0} "
+          f"end {kt[k + 1, 4] - t0}..{kt[k + 1, 5] - t0}")
