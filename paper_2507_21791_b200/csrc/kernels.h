@@ -187,10 +187,7 @@ cudaError_t small_launch(const SmallParams& p, cudaStream_t st, int* launches);
 struct ReduceArgs;
 ReduceArgs reduce_args(const TileParams& p, int ctas, double* out, int ld_out);
 bool small_mergeable(const SmallParams& p);
-// reduce_step4_kernel's per-block row partials live after the 64-byte ticket word:
-// the ticket buffer must hold 64 + 8 * kRowPart * kRowPartBlocks bytes
-constexpr int kRowPartBlocks = 1024;
-constexpr size_t kTicketBytes = 64 + 8 * 37 * (size_t)kRowPartBlocks;
+
 cudaError_t gram_reduce_launch_args(const ReduceArgs& a, int entries, cudaStream_t st,
                                     int* launches);
 cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallParams& p,

@@ -26,9 +26,7 @@ struct ReduceArgs {
 // returns (the block barrier inside is reached by all of them).  A CTA may run several
 // entry blocks in a row: the barrier at entry protects the shared slice sums of the
 // previous one.
-// vals (optional, shared): the block's RED_ENTRIES reduced values (0 for padding entries),
-// complete after a __syncthreads (reduce_step4_kernel's row work reads them).
-BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b, double* vals = nullptr) {
+BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b) {
   __shared__ double2 red[RED_SLICES][RED_ENTRIES];
   const int le = threadIdx.x % RED_ENTRIES, sl = threadIdx.x / RED_ENTRIES;
   const int idx = b * RED_ENTRIES + le;
@@ -55,7 +53,6 @@ BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b, double* vals = nullptr
   __syncthreads();
   red[sl][le] = make_double2(s, e);
   __syncthreads();
-  if (vals && sl == 0 && idx >= per_cta) vals[le] = 0.0;
   if (sl != 0 || idx >= per_cta) return;
   s = 0.0;
   e = 0.0;
@@ -66,7 +63,6 @@ BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b, double* vals = nullptr
     s = s2;
     e += err + v.y;
   }
-  if (vals) vals[le] = s + e;
   const int n = idx % a.N8;
   const int i = (idx / a.N8) % 8;
   const int t = idx / (8 * a.N8);

@@ -184,16 +184,7 @@ struct DBuf {
     o.p = nullptr;
     o.bytes = 0;
   }
-  DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) {
-      release();
-      p = o.p;
-      bytes = o.bytes;
-      o.p = nullptr;
-      o.bytes = 0;
-    }
-    return *this;
-  }
+  DBuf& operator=(DBuf&&) = delete;
   ~DBuf() { release(); }  // temporaries are freed on every exit path (Fail included)
   void ensure(size_t b) {
     if (b <= bytes) return;
@@ -550,7 +541,7 @@ class Runner {
     c->status.ensure(sizeof(DevStatus));
     status = reinterpret_cast<DevStatus*>(c->status.p);
     CUDA_OK(cudaMemsetAsync(status, 0, sizeof(DevStatus), c->stream));
-    c->ticket.ensure(kTicketBytes);
+    c->ticket.ensure(64);
     CUDA_OK(cudaMemsetAsync(c->ticket.p, 0, 64, c->stream));
     c->R.ensure((size_t)m * m * sizeof(double));
     CUDA_OK(cudaMemsetAsync(c->R.p, 0, (size_t)m * m * sizeof(double), c->stream));

@@ -444,7 +444,6 @@ constexpr int kStepThreads = 256;
 constexpr int kStepRowsMax = 2 * kStepThreads;  // small_mergeable: kp <= 512
 constexpr int kStepChunks = 7;                  // 36 x 7 = 252 product threads
 constexpr int kYZLd = kStepRowsMax + 1;         // odd column stride: columns in distinct banks
-constexpr int kRowPart = 37;                    // per-block row partials: 36 products + flag
 
 // (left, right) staged columns of product e: packed upper Y^T Y (10), full Y^T Z (16),
 // packed upper Z^T Z (10); columns 0..3 are Y, 4..7 are Z
@@ -462,40 +461,13 @@ BGS_DEV void product_cols(int e, int& cu, int& cv) {
   cv = j + (zz ? 4 : 0);
 }
 
-// Upper Cholesky of the symmetrized s x s block a (column-major 4 x 4) into g (shared),
-// on lanes 0..3 of one warp; every lane returns the same 1-based failing pivot (0 = ok).
-// Entry (i, j) = (0.5 (a_ij + a_ji) - sum_{k<i} g_ki g_kj) / g_ii, diagonal by sqrt --
-// the chol_warp expression; rows are finished in order, so the first failing pivot is
-// the same as in the column-ordered loop.
-BGS_DEV int chol4_lanes(const double* a, int s, double* g, int lane) {
-  if (lane < 16) g[lane] = 0.0;
-  __syncwarp();
-  for (int i = 0; i < s; ++i) {
-    double d = 0.0;
-    if (lane == i) {
-      double acc = 0.5 * (a[i + 4 * i] + a[i + 4 * i]);
-      for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * g[k + 4 * i];
-      d = acc;
-    }
-    d = __shfl_sync(0xffffffffu, d, i);
-    if (!(d > 0.0)) return i + 1;
-    const double gii = sqrt(d);
-    if (lane > i && lane < s) {
-      const int j = lane;
-      double acc = 0.5 * (a[i + 4 * j] + a[j + 4 * i]);
-      for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * g[k + 4 * j];
-      g[i + 4 * j] = acc / gii;
-    }
-    if (lane == i) g[i + 4 * i] = gii;
-    __syncwarp();
-  }
-  return 0;
-}
-
-// The same two routines with the factors in registers and the cross-lane operands moved by
-// shuffles (no shared-memory round trips on the chain): lane j < 4 owns column j.  Same
-// expressions and k order as chol4_lanes / trsm4_lanes, so the same bits.  The results are
-// also written to g / w in shared memory (column-major 4 x 4) for the later consumers.
+// Upper Cholesky of the symmetrized s x s block a (column-major 4 x 4, shared) on lanes
+// 0..3 of one warp, lane j owning column j, the factor in registers and the cross-lane
+// operands moved by shuffles (no shared-memory round trip on the chain: 1.7 -> 1.1 us per
+// factorization, %globaltimer stamps).  Entry (i, j) = (0.5 (a_ij + a_ji) -
+// sum_{k<i} g_ki g_kj) / g_ii, diagonal by sqrt -- chol_warp's expression and k order --,
+// rows finished in order, so the first failing pivot (1-based, returned on every lane) is
+// the column-ordered loop's.  The factor also goes to g in shared memory (4 x 4).
 BGS_DEV int chol4_reg(const double* a, int s, double* g, int lane) {
   const int j = lane & 3;
   double c[4], gc[4];  // symmetrized column j (entries i <= j), factor column j
@@ -534,8 +506,9 @@ BGS_DEV int chol4_reg(const double* a, int s, double* g, int lane) {
   return piv;
 }
 
-// w = g^{-T} b, g upper in shared memory (4 x 4), b in shared memory; lane j < s solves
-// column j with g's columns fetched once (broadcast reads) and w in registers.
+// w = g^{-T} b (tri_solve_left_trans), g upper and b in shared memory (4 x 4); lane j < s
+// solves column j with g read once (broadcast) and w in registers; same expressions and
+// order as trsm_lt_warp.  Returns the 1-based index of a zero diagonal (SingularError).
 BGS_DEV int trsm4_reg(const double* g, const double* b, int s, double* w, int lane) {
   for (int i = 0; i < s; ++i)
     if (g[i + 4 * i] == 0.0) return i + 1;
@@ -560,24 +533,6 @@ BGS_DEV int trsm4_reg(const double* g, const double* b, int s, double* w, int la
   return 0;
 }
 
-// w = g^{-T} b (g upper, shared) column-parallel: lane j < s solves column j into w
-// (shared); every lane returns the same 1-based index of a zero diagonal (0 = ok).
-BGS_DEV int trsm4_lanes(const double* g, const double* b, int s, double* w, int lane) {
-  for (int i = 0; i < s; ++i)
-    if (g[i + 4 * i] == 0.0) return i + 1;
-  if (lane < 16) w[lane] = 0.0;
-  __syncwarp();
-  if (lane < s) {
-    const int j = lane;
-    for (int i = 0; i < s; ++i) {
-      double acc = b[i + 4 * j];
-      for (int k = 0; k < i; ++k) acc -= g[k + 4 * i] * w[k + 4 * j];
-      w[i + 4 * j] = acc / g[i + 4 * i];
-    }
-  }
-  __syncwarp();
-  return 0;
-}
 }  // namespace
 
 #ifdef BGS_STEP_STAMPS
@@ -596,12 +551,7 @@ BGS_DEV unsigned long long gtime() {
 #define STAMP(i)
 #endif
 
-// PRE: the reduce CTAs of reduce_step4_kernel already did the row work (R column,
-// scol_next, non-finite check) and left per-block partial products in `bpart`
-// ([nblk][kRowPart]); this CTA sums them in block order instead of passing over the rows.
-template <bool PRE>
-__device__ __forceinline__ void onesync_step4_body(const SmallParams& p, const double* bpart = nullptr,
-                                                   int nblk = 0) {
+__device__ __forceinline__ void onesync_step4_body(const SmallParams& p) {
   const int s = p.s, kp = p.kp, tid = threadIdx.x, lane = tid & 31;
   const int nz = p.has_next ? s : 0;  // Z columns present
   __shared__ double yz[8 * kYZLd];    // [Y | Z] rows 0..kp, column stride kYZLd
@@ -630,116 +580,93 @@ __device__ __forceinline__ void onesync_step4_body(const SmallParams& p, const d
     }
     blk[b][e] = v;
   }
-  if (PRE) {
-    // ---- 1'. products: fixed-order sum of the reduce CTAs' block partials ----
-    if (tid < 36 * kStepChunks) {
-      const int e = tid % 36, c = tid / 36;
-      const int len = (nblk + kStepChunks - 1) / kStepChunks;
-      const int b0 = c * len, b1 = min(nblk, b0 + len);
-      double a0 = 0.0, a1 = 0.0;
-      int b = b0;
-      for (; b + 1 < b1; b += 2) {
-        a0 += bpart[(size_t)b * kRowPart + e];
-        a1 += bpart[(size_t)(b + 1) * kRowPart + e];
-      }
-      if (b < b1) a0 += bpart[(size_t)b * kRowPart + e];
-      part[e][c] = a0 + a1;
-    } else {
-      int bad = 0;
-      for (int b = tid - 36 * kStepChunks; b < nblk; b += kStepThreads - 36 * kStepChunks)
-        bad |= bpart[(size_t)b * kRowPart + 36] != 0.0;
-      if (bad) atomicOr(&bad_flag, 1);
+  // ---- 1. one pass over rows: stage [Y | Z], R column, scol_next copy, non-finite check ----
+  // Every load of the pass is issued before the first store (one L2 round trip: the
+  // stores to scol_next could alias G as far as the compiler knows).
+  double y[2][4], z[2][4], sp[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = tid + h * kStepThreads;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      y[h][l] = (r < kp && l < s) ? p.G[r + (size_t)l * p.ldg] : 0.0;
+      z[h][l] = (r < kp && l < nz) ? p.G[r + (size_t)(s + l) * p.ldg] : 0.0;
+      sp[h][l] = (r < kp && l < s) ? p.scol_prev[r + (size_t)l * p.ld_scol_prev] : 0.0;
     }
-    __syncthreads();
-    STAMP(2)
-    STAMP(3)
-    if (dead) return;
-    if (bad_flag) {
-      if (tid == 0) set_status(p.status, ST_NON_FINITE, 0, p.k + 1, SITE_NONE, 0);
-      return;
-    }
-  } else {
-    // ---- 1. one pass over rows: stage [Y | Z], R column, scol_next copy, non-finite check ----
-    // Every load of the pass is issued before the first store (one L2 round trip: the
-    // stores to scol_next could alias G as far as the compiler knows).
-    double y[2][4], z[2][4], sp[2][4];
-  #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = tid + h * kStepThreads;
-  #pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        y[h][l] = (r < kp && l < s) ? p.G[r + (size_t)l * p.ldg] : 0.0;
-        z[h][l] = (r < kp && l < nz) ? p.G[r + (size_t)(s + l) * p.ldg] : 0.0;
-        sp[h][l] = (r < kp && l < s) ? p.scol_prev[r + (size_t)l * p.ld_scol_prev] : 0.0;
-      }
-    }
-    // the rest of the reduced Gram, for the non-finite check (rows kp..gm)
-    const int tail = (p.gm - kp) * p.gn;
-    const double tv = tid < tail ? p.G[kp + tid % (p.gm - kp) + (size_t)(tid / (p.gm - kp)) * p.ldg] : 0.0;
-    int bad = !isfinite(tv);
-    for (int e = tid + kStepThreads; e < tail; e += kStepThreads) {
-      const int r = kp + e % (p.gm - kp), c = e / (p.gm - kp);
-      bad |= !isfinite(p.G[r + (size_t)c * p.ldg]);
-    }
-    double rcol[2][4];
-  #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = tid + h * kStepThreads;
-  #pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        bad |= !isfinite(y[h][l]) | !isfinite(z[h][l]);
-        // R(r, kp + l) = S_prev(r, l) + sum_m Y(r, m) S_diag(m, l)
-        double a = 0.0;
-  #pragma unroll
-        for (int m2 = 0; m2 < 4; ++m2) a += y[h][m2] * sdp[m2 + 4 * l];
-        rcol[h][l] = l < s ? sp[h][l] + a : 0.0;
-      }
-      if (r < kp) {
-  #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          yz[l * kYZLd + r] = y[h][l];
-          yz[(4 + l) * kYZLd + r] = z[h][l];
-          if (l < nz) p.scol_next[r + (size_t)l * p.ld_scol_next] = z[h][l];
-        }
-      }
-    }
-    if (bad) atomicOr(&bad_flag, 1);
-    __syncthreads();
-    STAMP(2)
-    if (dead) return;
-    if (bad_flag) {
-      if (tid == 0) set_status(p.status, ST_NON_FINITE, 0, p.k + 1, SITE_NONE, 0);
-      return;
-    }
-  #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = tid + h * kStepThreads;
-      if (r < kp)
-  #pragma unroll
-        for (int l = 0; l < 4; ++l)
-          if (l < s) p.R[r + (size_t)(kp + l) * p.ldr] = rcol[h][l];
-    }
-    // ---- 2. the 36 products over 7 row chunks (fixed order) ----
-    if (tid < 36 * kStepChunks) {
-      const int e = tid % 36, c = tid / 36;
-      int cu, cv;
-      product_cols(e, cu, cv);
-      const int len = (kp + kStepChunks - 1) / kStepChunks;
-      const int r0 = c * len, r1 = min(kp, r0 + len);
-      const double* u = yz + cu * kYZLd;
-      const double* v = yz + cv * kYZLd;
-      double a0 = 0.0, a1 = 0.0;
-      int r = r0;
-      for (; r + 1 < r1; r += 2) {
-        a0 = fma(u[r], v[r], a0);
-        a1 = fma(u[r + 1], v[r + 1], a1);
-      }
-      if (r < r1) a0 = fma(u[r], v[r], a0);
-      part[e][c] = a0 + a1;
-    }
-    __syncthreads();
-    STAMP(3)
   }
+  // the rest of the reduced Gram, for the non-finite check (rows kp..gm)
+  const int tail = (p.gm - kp) * p.gn;
+  const double tv = tid < tail ? p.G[kp + tid % (p.gm - kp) + (size_t)(tid / (p.gm - kp)) * p.ldg] : 0.0;
+  int bad = !isfinite(tv);
+  for (int e = tid + kStepThreads; e < tail; e += kStepThreads) {
+    const int r = kp + e % (p.gm - kp), c = e / (p.gm - kp);
+    bad |= !isfinite(p.G[r + (size_t)c * p.ldg]);
+  }
+  double rcol[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = tid + h * kStepThreads;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      bad |= !isfinite(y[h][l]) | !isfinite(z[h][l]);
+      // R(r, kp + l) = S_prev(r, l) + sum_m Y(r, m) S_diag(m, l)
+      double a = 0.0;
+#pragma unroll
+      for (int m2 = 0; m2 < 4; ++m2) a += y[h][m2] * sdp[m2 + 4 * l];
+      rcol[h][l] = l < s ? sp[h][l] + a : 0.0;
+    }
+    if (r < kp) {
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        yz[l * kYZLd + r] = y[h][l];
+        yz[(4 + l) * kYZLd + r] = z[h][l];
+        if (l < nz) p.scol_next[r + (size_t)l * p.ld_scol_next] = z[h][l];
+      }
+    }
+  }
+  if (bad) atomicOr(&bad_flag, 1);
+  __syncthreads();
+  STAMP(2)
+  if (dead) return;
+  if (bad_flag) {
+    if (tid == 0) set_status(p.status, ST_NON_FINITE, 0, p.k + 1, SITE_NONE, 0);
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = tid + h * kStepThreads;
+    if (r < kp)
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        if (l < s) p.R[r + (size_t)(kp + l) * p.ldr] = rcol[h][l];
+  }
+  // ---- 2. the 36 products: row pairs (2b, 2b + 1) summed in kStepChunks contiguous
+  // chunks of pairs, even / odd pairs interleaved (the merged path's order) ----
+  if (tid < 36 * kStepChunks) {
+    const int e = tid % 36, c = tid / 36;
+    int cu, cv;
+    product_cols(e, cu, cv);
+    const int np = (kp + 1) / 2;
+    const int len = (np + kStepChunks - 1) / kStepChunks;
+    const int b0 = c * len, b1 = min(np, b0 + len);
+    const double* u = yz + cu * kYZLd;
+    const double* v = yz + cv * kYZLd;
+    auto pair = [&](int b) {  // rows past kp are zero in yz (staged as 0 when r >= kp)
+      const double p0 = __dmul_rn(u[2 * b], v[2 * b]);
+      const double p1 = 2 * b + 1 < kp ? __dmul_rn(u[2 * b + 1], v[2 * b + 1]) : 0.0;
+      return __dadd_rn(p0, p1);
+    };
+    double a0 = 0.0, a1 = 0.0;
+    int b = b0;
+    for (; b + 1 < b1; b += 2) {
+      a0 = __dadd_rn(a0, pair(b));
+      a1 = __dadd_rn(a1, pair(b + 1));
+    }
+    if (b < b1) a0 = __dadd_rn(a0, pair(b));
+    part[e][c] = a0 + a1;
+  }
+  __syncthreads();
+  STAMP(3)
   if (tid >= 32) return;
   for (int e = lane; e < 36; e += 32) {  // lanes 0..3 also take products 32..35
     double t = 0.0;
@@ -831,63 +758,7 @@ __device__ __forceinline__ void onesync_step4_body(const SmallParams& p, const d
 }
 
 __global__ void __launch_bounds__(kStepThreads, 1) onesync_step4_kernel(SmallParams p) {
-  onesync_step4_body<false>(p);
-}
-
-// The row work of the one-sync step for the rows of entry block b (16 entries = 2 compact
-// Gram rows x 8 columns, reduce.cuh's layout with N8 = 8), done by the reduce CTA that just
-// reduced them: for rows r < kp the R column S_prev(r, :) + Y(r, :) S_diag (bcgs.cpp:332),
-// the copy of Z(r, :) into the next scol (:344), the 36 products of Y^T Y, Y^T Z, Z^T Z
-// restricted to these rows, and the non-finite check of every entry (dense_kernels.cpp:45-47)
-// -> bpart[b][0..35], bpart[b][36] = 1 if any entry is not finite.
-BGS_DEV void step4_rows(const ReduceArgs& a, int b, const SmallParams& p, const double* vals,
-                        double* bpart) {
-  __shared__ double pr[2][36];
-  __shared__ int badr[2];
-  const int s = p.s, kp = p.kp, tid = threadIdx.x;
-  const int nz = p.has_next ? s : 0;
-  if (tid < 2) {
-    const int idx0 = (b * RED_ENTRIES) / a.N8 + tid;  // row-in-tiles index t * 8 + i
-    const int t = idx0 / 8, i = idx0 % 8;
-    int row = -1;
-    if (t < a.ubox0) {
-      if (8 * t + i < a.lcols0) row = 8 * t + i;
-    } else if (8 * (t - a.ubox0) + i < a.lcols1) {
-      row = a.lcols0 + 8 * (t - a.ubox0) + i;
-    }
-    const double* v = vals + tid * a.N8;
-    int bad = 0;
-    for (int n = 0; n < a.N; ++n) bad |= row >= 0 && !isfinite(v[n]);
-    badr[tid] = bad;
-    double yz[8];
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      yz[l] = (row >= 0 && row < kp && l < s) ? v[l] : 0.0;
-      yz[4 + l] = (row >= 0 && row < kp && l < nz) ? v[s + l] : 0.0;
-    }
-#pragma unroll
-    for (int e = 0; e < 36; ++e) {
-      int cu, cv;
-      product_cols(e, cu, cv);
-      pr[tid][e] = yz[cu] * yz[cv];
-    }
-    if (row >= 0 && row < kp) {
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        if (l < s) {
-          double acc = 0.0;
-#pragma unroll
-          for (int m2 = 0; m2 < 4; ++m2)
-            if (m2 < s) acc += yz[m2] * p.sdiag[m2 + s * l];
-          p.R[row + (size_t)(kp + l) * p.ldr] = p.scol_prev[row + (size_t)l * p.ld_scol_prev] + acc;
-        }
-        if (l < nz) p.scol_next[row + (size_t)l * p.ld_scol_next] = yz[4 + l];
-      }
-    }
-  }
-  __syncthreads();
-  if (tid < 36) bpart[(size_t)b * kRowPart + tid] = pr[0][tid] + pr[1][tid];
-  if (tid == 36) bpart[(size_t)b * kRowPart + 36] = (badr[0] | badr[1]) ? 1.0 : 0.0;
+  onesync_step4_body(p);
 }
 
 // gram_reduce + the one-sync step in one launch: every CTA reduces its slice of the Gram,
@@ -895,8 +766,7 @@ BGS_DEV void step4_rows(const ReduceArgs& a, int b, const SmallParams& p, const 
 // Gram (the threadfence-reduction pattern); it also re-arms the ticket for the next launch.
 static_assert(RED_THREADS == kStepThreads, "one block shape for both halves");
 __global__ void __launch_bounds__(kStepThreads, 1)
-    reduce_step4_kernel(const ReduceArgs r, int nblk, SmallParams p, unsigned* ticket,
-                        double* bpart) {
+    reduce_step4_kernel(const ReduceArgs r, int nblk, SmallParams p, unsigned* ticket) {
   __shared__ int last;
   // The next fused kernel may launch now (programmatic dependent): its CTAs take the SMs
   // this grid frees and prefetch their first stages; they wait for this grid to complete
@@ -905,12 +775,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 #ifdef BGS_STEP_STAMPS
   const unsigned long long t_in = gtime();
 #endif
-  __shared__ double vals[RED_ENTRIES];
-  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
-    gram_reduce_body(r, b, vals);
-    __syncthreads();
-    step4_rows(r, b, p, vals, bpart);
-  }
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) gram_reduce_body(r, b);
 #ifdef BGS_STEP_STAMPS
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -926,7 +791,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   __threadfence();
   if (threadIdx.x == 0) *ticket = 0u;
   STAMP(1)
-  onesync_step4_body<true>(p, bpart, nblk);
+  onesync_step4_body(p);
 }
 
 bool small_mergeable(const SmallParams& p) {
@@ -939,10 +804,7 @@ cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallPar
   // one wave: the step body needs ~140 registers, so one CTA per SM; extra entry blocks
   // are looped over inside the CTA instead of running as a second wave
   const int nblk = (entries + RED_ENTRIES - 1) / RED_ENTRIES;
-  if (r.N8 != 8 || nblk > kRowPartBlocks) return cudaErrorInvalidValue;
-  // per-block row partials after the ticket word (the runtime sizes the buffer)
-  double* bpart = reinterpret_cast<double*>(reinterpret_cast<char*>(ticket) + 64);
-  reduce_step4_kernel<<<std::min(nblk, sms), kStepThreads, 0, st>>>(r, nblk, p, ticket, bpart);
+  reduce_step4_kernel<<<std::min(nblk, sms), kStepThreads, 0, st>>>(r, nblk, p, ticket);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
