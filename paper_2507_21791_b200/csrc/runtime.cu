@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <random>
 #include <string>
 #include <vector>
@@ -274,6 +275,25 @@ struct bgs_ctx {
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
   std::vector<DBuf> rscr;    // per-shard right-operand scratch of chunked Grams
   DBuf ticket;               // last-CTA ticket of the merged reduce + step kernel
+  // CUDA graphs of whole factorizations (bgs_factor_device): one per call signature,
+  // captured on the second call with that signature (the first sizes every workspace),
+  // replayed after; dropped when a workspace was reallocated since the capture.
+  struct GraphEntry {
+    std::string key;
+    std::vector<void*> bufs;  // workspace pointers the graph was captured with
+    cudaGraphExec_t exec = nullptr;
+    std::unique_ptr<bgs_stats> stats;
+    long launches = 0;
+    std::unique_ptr<HBuf> bounds;
+    int uses = 0;
+  };
+  std::vector<GraphEntry> graphs;
+  std::vector<std::string> seen;  // signatures run once (the next call captures)
+  std::vector<void*> buf_signature() const {
+    return {partial.p, G.p, scolA.p, scolB.p, sdiag.p, ydiag.p, save.p, r1.p, r2.p, rtop.p, R.p,
+            status.p, tsqr_ws.p, tsqr_bounds.p, roots.p, roots_all.p, cross_ws.p, cross_m.p,
+            ticket.p, metrics.p};
+  }
   int launches = 0;
   // live profiler: event pairs per launch, resolved after the stream syncs
   struct ProfClass {
@@ -329,6 +349,8 @@ struct bgs_ctx {
       event_pool.push_back(p.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
@@ -413,6 +435,7 @@ class Runner {
   std::vector<Shard> sh;
   bgs_stats* stats;
   const bgs_options* opt;  // BcgsOptions (probe)
+  HBuf* bounds_sink = nullptr;  // graph capture: pinned home of the TSQR leaf bounds
   long words = 0;
   DevStatus* status;
   int tsqr_L = 0;  // total leaves across local shards
@@ -577,7 +600,13 @@ class Runner {
     tsqr_L = leaf;
     c->tsqr_ws.ensure(tsqr_ws_bytes(tsqr_L, (int)s) + 64);
     c->tsqr_bounds.ensure(bounds.size() * sizeof(long));
-    CUDA_OK(cudaMemcpyAsync(c->tsqr_bounds.p, bounds.data(), bounds.size() * sizeof(long),
+    const void* bsrc = bounds.data();
+    if (bounds_sink) {  // graph capture: the copy node must read memory that outlives the call
+      bounds_sink->ensure(bounds.size() * sizeof(long) + 64);
+      memcpy(bounds_sink->p, bounds.data(), bounds.size() * sizeof(long));
+      bsrc = bounds_sink->p;
+    }
+    CUDA_OK(cudaMemcpyAsync(c->tsqr_bounds.p, bsrc, bounds.size() * sizeof(long),
                             cudaMemcpyHostToDevice, c->stream));
     c->roots.ensure((size_t)sh.size() * ss * sizeof(double) + 64);
     c->roots_all.ensure((size_t)P * ss * sizeof(double) + 64);
@@ -2152,13 +2181,96 @@ int bgs_factor_device_opts(bgs_ctx* c, int variant, long n, long m, long s, long
     sh.ldq = ldq;
     run.sh.push_back(sh);
     c->launches = 0;
+    // The whole factorization is one CUDA graph on repeated calls (BGS_GRAPH=0: plain
+    // launches).  Not with a host communicator (its exchanges synchronize), a probe, or
+    // the profilers.
+    const char* eg = getenv("BGS_GRAPH");
+    const bool graphable = !(eg && *eg == '0') && !c->hc_fn && !(opts && opts->probe) &&
+                           !c->prof_on && !run.tile_prof && !run.prof_step;
+    std::string key;
+    if (graphable) {
+      char kb[512];
+      snprintf(kb, sizeof kb, "%d %ld %ld %ld %ld %ld %p %ld %p %ld %d | %d %d %d %d %d %d %d %d",
+               variant, n, m, s, row0, n_local, (const void*)d_x, ldx, (void*)d_q, ldq,
+               opts ? opts->classic_intra : 0, run.no_fuse, run.no_k12c, run.gram_max_units,
+               run.no_merge_small, run.no_pdl, run.comp_mode, run.no_k2m, run.tile_dbg);
+      key = kb;
+      for (const char* ev : {"BGS_K12C_PLAN", "BGS_K12C_MAXS", "BGS_K12C_MINS", "BGS_UPDATE_MAXKP",
+                             "BGS_TSQR_GENERIC", "BGS_K2_SCALAR"}) {
+        const char* v = getenv(ev);
+        key += std::string(" ") + (v ? v : "-");
+      }
+    }
+    auto body = [&]() {
+      // For s not a multiple of 4 the fused kernel's last k-step reads a few Q columns that
+      // are not computed yet (zero coefficients): they must hold finite values.
+      if (s % 4 && n_local > 0)
+        CUDA_OK(cudaMemset2DAsync(d_q, ldq * sizeof(double), 0, n_local * sizeof(double), m,
+                                  c->stream));
+      run.run();
+    };
+    bgs_ctx::GraphEntry* ge = nullptr;
+    if (graphable) {
+      for (auto& g : c->graphs)
+        if (g.key == key) ge = &g;
+      if (ge && ge->bufs != c->buf_signature()) {  // a workspace moved: capture again
+        cudaGraphExecDestroy(ge->exec);
+        c->graphs.erase(c->graphs.begin() + (ge - c->graphs.data()));
+        ge = nullptr;
+      }
+      if (!ge && std::find(c->seen.begin(), c->seen.end(), key) != c->seen.end()) {
+        // second call with this signature: capture (every workspace is sized already)
+        if (c->graphs.size() >= 8) {
+          cudaGraphExecDestroy(c->graphs.front().exec);
+          c->graphs.erase(c->graphs.begin());
+        }
+        c->graphs.emplace_back();
+        bgs_ctx::GraphEntry& g = c->graphs.back();
+        g.key = key;
+        g.stats.reset(new bgs_stats());
+        g.bounds.reset(new HBuf());
+        // (pinned memory cannot be allocated while capturing: size it for the leaf plan
+        // of setup(), at most ceil(rows / 256) leaves + 1 bounds)
+        g.bounds->ensure(((size_t)(n_local + 255) / 256 + 4) * sizeof(long) + 64);
+        run.stats = g.stats.get();
+        run.bounds_sink = g.bounds.get();
+        cudaGraph_t graph = nullptr;
+        CUDA_OK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          body();
+        } catch (...) {
+          cudaStreamEndCapture(c->stream, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          c->graphs.pop_back();
+          throw;
+        }
+        CUDA_OK(cudaStreamEndCapture(c->stream, &graph));
+        const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) {
+          c->graphs.pop_back();
+          fail(BGS_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+        }
+        g.launches = c->launches;
+        g.bufs = c->buf_signature();
+        ge = &g;
+        run.stats = stats;
+      }
+    }
     CUDA_OK(cudaEventRecord(c->e0, c->stream));
-    // For s not a multiple of 4 the fused kernel's last k-step reads a few Q columns that
-    // are not computed yet (zero coefficients): they must hold finite values.
-    if (s % 4 && n_local > 0)
-      CUDA_OK(cudaMemset2DAsync(d_q, ldq * sizeof(double), 0, n_local * sizeof(double), m,
-                                c->stream));
-    run.run();
+    if (ge) {
+      run.status = reinterpret_cast<DevStatus*>(c->status.p);  // (set by setup() otherwise)
+      CUDA_OK(cudaGraphLaunch(ge->exec, c->stream));
+      ge->uses += 1;
+      if (stats) memcpy(stats, ge->stats.get(), sizeof *stats);
+      c->launches = (int)ge->launches;
+    } else {
+      body();
+      if (graphable && std::find(c->seen.begin(), c->seen.end(), key) == c->seen.end()) {
+        if (c->seen.size() >= 64) c->seen.erase(c->seen.begin());
+        c->seen.push_back(key);
+      }
+    }
     CUDA_OK(cudaEventRecord(c->e1, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
     CUDA_OK(cudaGetLastError());

@@ -907,3 +907,51 @@ def test_classic_cholqr_not_spd_diagnostic(gpu_ctx):
     assert ref.rc == 2 and not out.ok
     assert out.error == ref.msg, (out.error, ref.msg)
     assert out.not_spd_pivot == ref.pivot == 3
+
+
+# ---------------------------------------------------------------------------------------
+# CUDA-graph replay of whole factorizations (bgs_factor_device, second call on: captured,
+# then replayed): bitwise the same factors and accounting as plain launches, failures
+# reported the same way from a replay, recapture after a workspace grew.
+# ---------------------------------------------------------------------------------------
+def test_graph_replay_is_bitwise_identical(monkeypatch):
+    import torch
+
+    import paper_2507_21791_b200 as bgs
+    ctx = bgs.Context(0)
+    for (n, m, s, v) in [(20000, 64, 4, 3), (20000, 64, 8, 4), (5000, 48, 3, 5), (3000, 64, 16, 1)]:
+        ld = (n + 31) // 32 * 32
+        X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
+        bgs.gen_gaussian_device(ctx, 7, 0, n, m, X.data_ptr(), ld)
+        outs = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("BGS_GRAPH", mode)
+            for _ in range(3):  # plain, capture, replay
+                Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+                r, st, tm = bgs.factor_device(ctx, v, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+                outs.setdefault(mode, []).append((r, Q.cpu().numpy(), st.sync_count,
+                                                  list(st.event_labels), st.words_reduced))
+        base = outs["0"][0]
+        for r, q, sc, lab, w in outs["0"] + outs["1"]:
+            assert np.array_equal(r, base[0]) and np.array_equal(q, base[1])
+            assert (sc, lab, w) == base[2:]
+
+
+def test_graph_replay_reports_not_spd(oracle):
+    import torch
+
+    import paper_2507_21791_b200 as bgs
+    ctx = bgs.Context(0)
+    n, m, s = 2000, 32, 4
+    x = oracle.gen_matrix(n, m, s, 1e12, 5, False)
+    ld = (n + 31) // 32 * 32
+    X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    X[:, :n] = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    for _ in range(4):
+        Q = torch.zeros_like(X)
+        with pytest.raises(bgs.api.NotSpdError, match="BCGSI\\+P-1S: "):
+            bgs.factor_device(ctx, 3, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+    # and a healthy call on the same context afterwards
+    bgs.gen_gaussian_device(ctx, 1, 0, n, m, X.data_ptr(), ld)
+    r, st, _ = bgs.factor_device(ctx, 3, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+    assert st.sync_count == m // s and np.all(np.diag(r) > 0)
