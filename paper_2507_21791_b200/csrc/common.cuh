@@ -12,6 +12,25 @@
 
 #define BGS_DEV __device__ __forceinline__
 
+// Checked builds (make checked -> _lib_chk/libbgs_gpu.so, -DBGS_CHECKED): device-side
+// bounds checks on the index arithmetic of the hot kernels, trapping with a message.  The
+// pool's compute-sanitizer is closed (it left GPUs needing a reset), so these, the
+// NaN-poisoned buffers (BGS_POISON) and the fuzzer stand in for memcheck.
+#ifdef BGS_CHECKED
+#define BGS_DCHECK(cond, what)                                                              \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("[bgs check] %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x, what);                                                           \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define BGS_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace bgs {
 
 // ---------------------------------------------------------------------------------

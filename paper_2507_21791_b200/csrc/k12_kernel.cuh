@@ -120,6 +120,19 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
   __shared__ double ep_t[2][16], ep_s2[16], ep_ai[16], ep_bi[16], ep_w[16], ep_m[64];
 
   const uint32_t rank = pair ? cluster_ctarank() : 0u, peer = rank ^ 1u;
+#ifdef BGS_CHECKED
+  // every stage slot, the reduction and exchange buffers and the barriers inside the
+  // dynamic allocation (the host sized it with k12_smem_bytes)
+  {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const size_t need = (size_t)(smem - smem_raw) + (size_t)S * slot_bytes + kRedBytes +
+                        (pair ? xchg_bytes(R) : 0) + (2 * S + 4) * sizeof(uint64_t);
+    BGS_DCHECK(need <= dyn, "k12: shared-memory layout exceeds the allocation");
+    BGS_DCHECK(p.own_n[rank] + p.ext_n[rank] + p.U1 <= p.slot_units, "k12: units exceed the slot");
+    BGS_DCHECK(S >= 1 && S <= kMaxStages, "k12: ring depth");
+  }
+#endif
   const int own_u0 = p.own_u0[rank], own_n = p.own_n[rank];
   const int ext_u0 = p.ext_u0[rank], ext_n = p.ext_n[rank];
   const int nloc = own_n + ext_n + p.U1;
@@ -186,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
                 mp = &p.map1[wi - 3];
               }
               const int wu = 16 >> wi;
+              BGS_DCHECK(u + wu <= p.slot_units, "k12: TMA box past the stage slot");
               tma_load_3d(dst + (size_t)u * kUnitChunkBytes, mp, &full[slot], 0, rb, c);
               u += wu;
               c += 8 * wu;
@@ -516,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
           if (on && c < s) {
             const double v = e ? o1 : o0;
             if (sstore) sts64(cb + elem_off<2>(lcol + c, erow), v);
+            BGS_DCHECK(!gstore || (grow < p.n_rows && c < s), "k12: epilogue store outside the shard");
             if (gstore) gdst[grow + (size_t)c * gld] = v;
           }
         }
@@ -603,6 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
             const double2 o = lds128(park + (uint32_t)((((w * MTW + jj) * 2 + e) * 32 + lane) * 16));
             double sm, err;
             two_sum(hi[jj][e], o.x, sm, err);
+            BGS_DCHECK(tg < p.mt_out, "k12: partial tile outside the slot");
             part[((size_t)tg * 8 + ii) * 8 + 2 * kk + e] = make_double2(sm, err + (lo[jj][e] + o.y));
           }
         }

@@ -76,6 +76,7 @@ BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b) {
     if (r >= a.lcols1) return;
     row = a.lcols0 + r;
   }
+  BGS_DCHECK(row < a.M && n < a.N, "gram_reduce: output entry outside the Gram");
   a.out[row + (size_t)n * a.M] = s + e;
 }
 

@@ -101,6 +101,15 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   uint64_t* dempty = dfull + kUmBufs;              // [kUmBufs]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long nblk = p.total_blocks;
+#ifdef BGS_CHECKED
+  {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    BGS_DCHECK(reinterpret_cast<unsigned char*>(dempty + kUmBufs) - smem_raw <= (long)dyn,
+               "k2m: shared-memory layout exceeds the allocation");
+    BGS_DCHECK(kp % 8 == 0 && NS >= 3 && NS <= kUmStagesMax, "k2m: kp / ring depth");
+  }
+#endif
   const long b0 = (long)blockIdx.x * nblk / gridDim.x;
   const long b1 = (long)(blockIdx.x + 1) * nblk / gridDim.x;
 
@@ -184,6 +193,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
           while (done < w) {  // greedy boxes {16, 4, 32 / 16 / 8}: 512-byte runs per column
             const int left = w - done;
             const int wi = left >= 32 ? 2 : left >= 16 ? 3 : 4;
+            BGS_DCHECK(done + (128 >> wi) <= kUmKC, "k2m: TMA box past the stage");
             tma_load_3d(dst + (size_t)done * 512, &p.map[wi], &full[slot], 0, (int)(4 * b),
                         p.col0 + c0 + done);
             done += 128 >> wi;

@@ -1,7 +1,8 @@
 # One-off parity check at the headline shape (BASELINE config 2: BCGSI+P-1S, n=1e6, m=400,
 # s=4, i.i.d. N(0,1), seed 12345): the UNMODIFIED reference (oracle/_ref, all host threads)
 # and this library on the same X bits; R compared entrywise, LOO and residual of both Q
-# measured with the same device metrics (double-double).  Writes gpurun_out/config2_parity.json.
+# measured with the same device metrics (double-double).  Writes gpurun_out/config2_parity.json
+# and the golden fixture gpurun_out/config2_ref.npz (-> tests/golden/, test_gpu_config2.py).
 #   python tools/config2_parity.py      (one B200 box; ~6 min, mostly the reference)
 import json, os, sys, time
 sys.path.insert(0, ".")
@@ -45,4 +46,8 @@ rep = {
 }
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(rep, open("gpurun_out/config2_parity.json", "w"), indent=1)
+# golden fixture for tests/test_gpu_config2.py: the reference's R and accounting at config 2
+np.savez_compressed("gpurun_out/config2_ref.npz", r=rr.r, loo=loo_r, resid=res_r,
+                    sync_count=rr.sync_count, words=rr.words_reduced,
+                    labels=np.array(rr.labels), seconds=t_ref, procs=procs)
 print(json.dumps(rep, indent=1))
