@@ -233,6 +233,10 @@ cudaError_t copy_cols_launch(const double* src, long lds, double* dst, long ldd,
                              long cols, cudaStream_t st);
 // Sum of squares of (X - Q R) and of X, scaled by the host-supplied maxima, per-CTA
 // partials -> out[0..1] (double-double reduced).
+// ||A||_2 of a symmetric m x m device matrix (optionally A - I first, in place) by the
+// reference's power iteration on A^T A; ws >= 3 m + 8 doubles.  Synchronizes `st`.
+cudaError_t sym_two_norm(double* A, int m, bool sub_identity, double* ws, double* out,
+                         cudaStream_t st);
 cudaError_t residual_launch(const double* x, long ldx, const double* q, long ldq,
                             const double* r, long ldr, long n_rows, long m, double inv_scale_d,
                             double inv_scale_x, double* ws, double* out, int num_sms,

@@ -10,6 +10,9 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -190,6 +193,99 @@ cudaError_t residual_launch(const double* x, long ldx, const double* q, long ldq
                                                        reinterpret_cast<double2*>(ws));
   }
   dd_finish_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const double2*>(ws), (int)grid, out);
+  return cudaGetLastError();
+}
+
+// ---- two_norm on the device (metrics.cpp:8-14, dense_kernels.cpp:205-239) ----
+// y = A x for a symmetric m x m A (column-major): warp w of the CTA forms row i = 8 b + w as
+// the dot of column i with x (coalesced), x staged in shared memory.
+__global__ void __launch_bounds__(256) sym_matvec_kernel(const double* __restrict__ A, int m,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ y) {
+  extern __shared__ double xs[];
+  for (int k = threadIdx.x; k < m; k += blockDim.x) xs[k] = x[k];
+  __syncthreads();
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= m) return;
+  const double* col = A + (size_t)i * m;
+  double a0 = 0.0, a1 = 0.0;
+  int k = lane;
+  for (; k + 32 < m; k += 64) {
+    a0 = fma(col[k], xs[k], a0);
+    a1 = fma(col[k + 32], xs[k + 32], a1);
+  }
+  if (k < m) a0 = fma(col[k], xs[k], a0);
+  double acc = a0 + a1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[i] = acc;
+}
+
+// nrm = ||u||_2 (one CTA, fixed order); then v = u / nrm (a second launch reads nrm).
+__global__ void __launch_bounds__(256) norm2_kernel(const double* __restrict__ u, int m,
+                                                    double* __restrict__ nrm) {
+  __shared__ double red[8];
+  double a = 0.0;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) a = fma(u[k], u[k], a);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    nrm[0] = sqrt(t);
+  }
+}
+
+__global__ void scale_kernel(const double* __restrict__ u, int m, const double* __restrict__ nrm,
+                             double* __restrict__ v) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) v[k] = nrm[0] == 0.0 ? 0.0 : u[k] / nrm[0];
+}
+
+__global__ void sub_identity_kernel(double* A, int m) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) A[k + (size_t)k * m] -= 1.0;
+}
+
+// ||A||_2 of a symmetric device matrix by power iteration on A^T A = A A (the reference's
+// iteration: w = A^T A v, lambda = ||w||, v = w / lambda, stop when lambda moves by at most
+// 1e-10 relative, at most 5000 rounds): sqrt(lambda).  ws: 3 m + 8 doubles.
+cudaError_t sym_two_norm(double* A, int m, bool sub_identity, double* ws, double* out,
+                         cudaStream_t st) {
+  cudaError_t e;
+  if (sub_identity) sub_identity_kernel<<<(m + 255) / 256, 256, 0, st>>>(A, m);
+  double* v = ws;
+  double* w = ws + m;
+  double* u = ws + 2 * m;
+  double* nrm = ws + 3 * m;
+  std::vector<double> v0(m);
+  double nv = 0.0;
+  for (int i = 0; i < m; ++i) {
+    v0[i] = 1.0 + (double)(i % 13) / 16.0;
+    nv += v0[i] * v0[i];
+  }
+  nv = std::sqrt(nv);
+  for (auto& t : v0) t /= nv;
+  if ((e = cudaMemcpyAsync(v, v0.data(), (size_t)m * sizeof(double), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return e;
+  const size_t smem = (size_t)m * sizeof(double);
+  if ((e = ensure_smem(sym_matvec_kernel, smem)) != cudaSuccess) return e;
+  double lambda = 0.0, prev = 0.0;
+  for (int it = 0; it < 5000; ++it) {
+    sym_matvec_kernel<<<(m + 7) / 8, 256, smem, st>>>(A, m, v, w);
+    sym_matvec_kernel<<<(m + 7) / 8, 256, smem, st>>>(A, m, w, u);
+    norm2_kernel<<<1, 256, 0, st>>>(u, m, nrm);
+    scale_kernel<<<(m + 255) / 256, 256, 0, st>>>(u, m, nrm, v);
+    if ((e = cudaMemcpyAsync(&lambda, nrm, sizeof(double), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    if (lambda == 0.0) break;
+    if (it > 0 && std::fabs(lambda - prev) <= 1e-10 * lambda) break;
+    prev = lambda;
+  }
+  *out = std::sqrt(lambda);
   return cudaGetLastError();
 }
 

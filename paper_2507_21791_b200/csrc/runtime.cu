@@ -2347,8 +2347,8 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
     select_device(c);
     order_after_caller(c);
     (void)n;
-    const int si = 8;
-    // Q^T Q in panels of 8 right columns through K1 (+ NCCL allreduce)
+    const int si = 32;
+    // Q^T Q in panels of 32 right columns through K1 (+ allreduce), assembled on the device
     Runner run(c, BGS_BCGSI_PLUS_P_1S, std::max(n, m), m, 1, c->nranks, c->collective(), nullptr);
     Shard sh;
     sh.rows = n_local;
@@ -2362,49 +2362,23 @@ int bgs_metrics_device(bgs_ctx* c, long n, long m, long n_local, const double* d
     const size_t per_cta = gram_partial_doubles_per_cta((int)((m + 7) / 8) + 1, si);
     c->partial.ensure(per_cta * sizeof(double) * (size_t)run.grid_total() + 64);
     c->G.ensure((size_t)(m + 16) * 32 * sizeof(double) + 4096);
-    std::vector<double> gram((size_t)m * m), panel((size_t)m * si);
+    DBuf dgram, dws;
+    dgram.ensure((size_t)m * m * sizeof(double));
+    dws.ensure((size_t)(3 * m + 8) * sizeof(double));
     for (long j0 = 0; j0 < m; j0 += si) {
       const int nb = (int)std::min<long>(si, m - j0);
       GramSpec g = Runner::spec1(SQ, 0, (int)m, (int)m);
       run.add_right(g, 0, (int)j0, nb);
       run.gram(g, "", false, true);
-      CUDA_OK(cudaMemcpyAsync(panel.data(), c->G.p, (size_t)m * nb * sizeof(double),
-                              cudaMemcpyDeviceToHost, c->stream));
-      CUDA_OK(cudaStreamSynchronize(c->stream));
-      for (int jj = 0; jj < nb; ++jj)
-        for (long i = 0; i < m; ++i) gram[i + (size_t)(j0 + jj) * m] = panel[i + (size_t)jj * m];
+      CUDA_OK(cudaMemcpyAsync(dgram.d() + (size_t)j0 * m, c->G.p, (size_t)m * nb * sizeof(double),
+                              cudaMemcpyDeviceToDevice, c->stream));
     }
-    for (long i = 0; i < m; ++i) gram[i + i * m] -= 1.0;
-    // two_norm (dense_kernels.cpp:205-239): power iteration on a^T a
-    std::vector<double> ata((size_t)m * m);
-    for (long j = 0; j < m; ++j)
-      for (long i = 0; i < m; ++i) {
-        double acc = 0.0;
-        for (long k = 0; k < m; ++k) acc += gram[k + i * m] * gram[k + j * m];
-        ata[i + j * m] = acc;
-      }
-    std::vector<double> v(m), w(m);
-    double nv = 0.0;
-    for (long i = 0; i < m; ++i) { v[i] = 1.0 + (double)(i % 13) / 16.0; nv += v[i] * v[i]; }
-    nv = std::sqrt(nv);
-    for (auto& t : v) t /= nv;
-    double lambda = 0.0, lambda_prev = 0.0;
-    for (int it = 0; it < 5000; ++it) {
-      double nw = 0.0;
-      for (long i = 0; i < m; ++i) {
-        double acc = 0.0;
-        for (long k = 0; k < m; ++k) acc += ata[i + k * m] * v[k];
-        w[i] = acc;
-        nw += acc * acc;
-      }
-      nw = std::sqrt(nw);
-      if (nw == 0.0) { lambda = 0.0; break; }
-      lambda = nw;
-      for (long i = 0; i < m; ++i) v[i] = w[i] / nw;
-      if (std::fabs(lambda - lambda_prev) <= 1e-10 * lambda) break;
-      lambda_prev = lambda;
-    }
-    if (loo) *loo = std::sqrt(lambda);
+    // two_norm(Q^T Q - I) (dense_kernels.cpp:205-239) by power iteration on the device:
+    // O(m^2) per round instead of the O(m^3) host product it replaces (m = 4096 took minutes)
+    double lnorm = 0.0;
+    CUDA_OK(sym_two_norm(dgram.d(), (int)m, true, dws.d(), &lnorm, c->stream));
+    if (loo) *loo = lnorm;
+
     // residual
     // per-CTA (d^2, x^2) double-double partials: <= 2*sms CTAs x 2 double2, then 2 results
     const size_t part_doubles = (size_t)2 * c->sms * 4;

@@ -955,3 +955,34 @@ def test_graph_replay_reports_not_spd(oracle):
     bgs.gen_gaussian_device(ctx, 1, 0, n, m, X.data_ptr(), ld)
     r, st, _ = bgs.factor_device(ctx, 3, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
     assert st.sync_count == m // s and np.all(np.diag(r) > 0)
+
+
+@pytest.mark.parametrize("v", [3, 1], ids=lambda v: NAMES[v])
+def test_m4096_s16_limits(gpu_ctx, v):
+    """The largest shape validate() accepts (m = 4096, s = 16): chained K2m updates past
+    its coefficient panel, chunked Grams, unstaged small ops, the device two-norm."""
+    import time
+
+    import paper_2507_21791_b200 as bgs
+    x = bgs.gen_gaussian_host(11, 4200, 4096)
+    t = time.time()
+    out = bgs.run_factor(v, x, 16, 1, metrics=True, ctx=gpu_ctx)
+    assert out.ok, out.error
+    assert out.stats.sync_count == bgs.expected_syncs(v, 256)
+    assert_structure(out.r)
+    assert out.loo <= 1e-12 and out.resid <= 1e-14, (out.loo, out.resid)
+    assert time.time() - t < 120
+
+
+def test_device_two_norm_matches_exact_metric(oracle, gpu_ctx):
+    """The LOO of the device metrics (power iteration on the GPU) agrees with the exact
+    metric of the oracle (metrics.cpp:8-14) on Q's with visible loss of orthogonality."""
+    import paper_2507_21791_b200 as bgs
+    rng = np.random.default_rng(4)
+    for (n, m, eps) in [(3000, 96, 1e-6), (5000, 400, 1e-9), (700, 7, 1e-3)]:
+        q, _ = np.linalg.qr(rng.standard_normal((n, m)))
+        q = q + eps * rng.standard_normal((n, m))
+        r = np.triu(rng.standard_normal((m, m)))
+        loo, _ = bgs.loss_and_residual(q @ r, q, r, ctx=gpu_ctx)
+        exact = oracle.loo(q)
+        assert abs(loo - exact) <= 1e-6 * exact, (n, m, loo, exact)
