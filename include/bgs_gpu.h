@@ -106,6 +106,31 @@ int bgs_ctx_create(int device, int rank, int nranks, const void* nccl_unique_id,
 typedef int (*bgs_allgather_fn)(void* user, const void* send, void* recv, unsigned long bytes);
 int bgs_ctx_create_host_comm(int device, int rank, int nranks, bgs_allgather_fn fn, void* user,
                              bgs_ctx** out, bgs_error* err);
+/* A context whose collectives are ONE-SHOT exchanges over peer-mapped device memory
+ * (SURVEY.md 8(f) row 4): exact_allreduce (communicator.cpp:226-250) and the TSQR root
+ * exchange fused with its Gram allreduce (communicator.cpp:252-317) re-designed for GPUs
+ * that address each other's memory -- NVLink / NVSwitch P2P between the GPUs of a node, or
+ * CUDA IPC between processes.  Each rank owns a window [flags | 2 parities x nranks
+ * slots]; a sync is: every rank stores its partial into its slot of EVERY window and
+ * then publishes a flag there (release, system scope); every rank waits for the nranks
+ * flags of its own window and adds the partials in rank order (bitwise replicated R).
+ * One network traversal, no host round trip, no second phase.
+ *   bgs_ctx_create_peer   allocates the window (slot_bytes 0: sized for the largest
+ *                         exchange the library admits, 1 MiB per slot);
+ *   bgs_ctx_peer_handle   exports it (BGS_PEER_HANDLE_BYTES; ranks allgather these);
+ *   bgs_ctx_peer_attach   maps all nranks windows (handles in rank order).
+ * wait_mode 0 picks how a rank waits: 2 = an acquire spin at the head of the sum kernel
+ * when every rank has its own GPU; 1 = stream memory operations (cuStreamWaitValue32)
+ * when ranks share a GPU, where no kernel may wait on another rank's kernel.  */
+#define BGS_PEER_HANDLE_BYTES 128
+int bgs_ctx_create_peer(int device, int rank, int nranks, unsigned long slot_bytes, bgs_ctx** out,
+                        bgs_error* err);
+int bgs_ctx_peer_handle(bgs_ctx* ctx, void* handle, bgs_error* err);
+int bgs_ctx_peer_attach(bgs_ctx* ctx, const void* handles, int wait_mode, bgs_error* err);
+/* Protocol self-test on one GPU: nranks emulated ranks in this process, `epochs` exchanges
+ * of ng gathered + ns summed doubles; pushes, a device synchronize, then the spin flavour
+ * of the sum kernel (nothing ever waits); results checked bitwise. */
+int bgs_peer_selftest(int device, int nranks, long ng, long ns, int epochs, bgs_error* err);
 void bgs_ctx_destroy(bgs_ctx* ctx);
 int bgs_nccl_unique_id(void* out128, bgs_error* err); /* ncclGetUniqueId via the ctx's NCCL */
 /* The *_device entry points below run on the context's own stream and first wait (an

@@ -8,7 +8,8 @@ from .api import *  # noqa: F401,F403
 from .api import (  # noqa: F401
     BcgsOptions, Context, FactorOutcome, SyncStats, VariantId, all_variants, default_context,
     expected_syncs, factor_device, gen_gaussian_device, gen_gaussian_host, gen_matrix, gram,
-    loss_and_residual, metrics_device, nccl_unique_id, parse_variant, run_factor, shard_rows,
+    loss_and_residual, metrics_device, nccl_unique_id, parse_variant, peer_selftest, run_factor,
+    shard_rows,
     tsqr, variant_flops, variant_name,
 )
 
@@ -16,6 +17,7 @@ __all__ = [
     "BcgsOptions", "Context", "FactorOutcome", "SyncStats", "VariantId", "all_variants", "default_context",
     "expected_syncs", "factor_device", "gen_gaussian_device", "gen_gaussian_host", "gen_matrix",
     "gram",
-    "loss_and_residual", "metrics_device", "nccl_unique_id", "parse_variant", "run_factor",
+    "loss_and_residual", "metrics_device", "nccl_unique_id", "parse_variant", "peer_selftest",
+    "run_factor",
     "shard_rows", "tsqr", "variant_flops", "variant_name",
 ]

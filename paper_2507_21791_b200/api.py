@@ -163,6 +163,10 @@ def _load() -> ctypes.CDLL:
         "bgs_gen_matrix_host": ([L, L, L, D, ctypes.c_ulonglong, I, P, L, P], I),
         "bgs_factor_opts": ([P, I, L, L, L, I, P, L, P, L, P, L, P, P, P, P], I),
         "bgs_factor_device_opts": ([P, I, L, L, L, L, L, P, L, P, L, P, L, P, P, P, P], I),
+        "bgs_ctx_create_peer": ([I, I, I, ctypes.c_ulong, P, P], I),
+        "bgs_ctx_peer_handle": ([P, P, P], I),
+        "bgs_ctx_peer_attach": ([P, P, I, P], I),
+        "bgs_peer_selftest": ([I, I, L, L, I, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -181,7 +185,10 @@ EXPORTED_SYMBOLS = (
     "bgs_gen_gaussian_host", "bgs_metrics", "bgs_metrics_device", "bgs_gram", "bgs_tsqr",
     "bgs_profile_enable", "bgs_profile_read", "bgs_ctx_create_host_comm", "bgs_factor_opts",
     "bgs_factor_device_opts", "bgs_gen_matrix_host",
+    "bgs_ctx_create_peer", "bgs_ctx_peer_handle", "bgs_ctx_peer_attach", "bgs_peer_selftest",
 )
+
+PEER_HANDLE_BYTES = 128
 
 # bgs_allgather_fn / bgs_probe_fn (include/bgs_gpu.h)
 _ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
@@ -303,6 +310,15 @@ class FactorOutcome:
     timing: Timing = field(default_factory=Timing)
 
 
+def peer_selftest(device: int = 0, nranks: int = 4, ng: int = 16, ns: int = 3000,
+                  epochs: int = 5) -> None:
+    """bgs_peer_selftest: the one-shot exchange protocol with nranks emulated ranks on one
+    GPU (pushes, a device synchronize, then the spin flavour of the sum: nothing waits)."""
+    err = _Err()
+    _raise(_lib.bgs_peer_selftest(int(device), int(nranks), int(ng), int(ns), int(epochs),
+                                  ctypes.byref(err)), err)
+
+
 # ---------------------------------------------------------------------------------------
 # context
 # ---------------------------------------------------------------------------------------
@@ -315,15 +331,26 @@ class Context:
     ``host_allgather``: instead of NCCL, a blocking host allgather ``f(bytes) -> bytes``
     (every rank's payload concatenated in rank order), e.g. over torch.distributed gloo
     (``dist.host_allgather``).  Each sync is one call; partials are summed in rank order
-    on the host (bgs_ctx_create_host_comm).  Lets several ranks share one GPU."""
+    on the host (bgs_ctx_create_host_comm).  Lets several ranks share one GPU.
+
+    ``peer=True``: the one-shot exchange over peer-mapped device windows
+    (bgs_ctx_create_peer): after construction every rank passes ``peer_handle()`` of all
+    ranks, in rank order, to ``peer_attach`` (``dist.attach_peers`` does both over
+    torch.distributed).  No host round trip per sync; NVLink P2P between GPUs, CUDA IPC
+    between processes (which may also share one GPU: the wait is then a stream memory
+    operation, never a spinning kernel)."""
 
     def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1,
                  nccl_unique_id: Optional[bytes] = None,
-                 host_allgather: Optional[Callable[[bytes], bytes]] = None):
+                 host_allgather: Optional[Callable[[bytes], bytes]] = None,
+                 peer: bool = False, peer_slot_bytes: int = 0):
         self._h = ctypes.c_void_p()
         err = _Err()
         self._cb = None
-        if host_allgather is not None:
+        if peer:
+            rc = _lib.bgs_ctx_create_peer(int(device), int(rank), int(nranks), int(peer_slot_bytes),
+                                          ctypes.byref(self._h), ctypes.byref(err))
+        elif host_allgather is not None:
             def _ag(user, send, recv, nbytes, _f=host_allgather, _p=int(nranks)):
                 try:
                     out = _f(ctypes.string_at(send, nbytes))
@@ -349,6 +376,23 @@ class Context:
     @property
     def handle(self) -> ctypes.c_void_p:
         return self._h
+
+    def peer_handle(self) -> bytes:
+        """This rank's window handle (BGS_PEER_HANDLE_BYTES) for the other ranks."""
+        buf = ctypes.create_string_buffer(PEER_HANDLE_BYTES)
+        err = _Err()
+        _raise(_lib.bgs_ctx_peer_handle(self._h, buf, ctypes.byref(err)), err)
+        return buf.raw
+
+    def peer_attach(self, handles, wait_mode: int = 0) -> None:
+        """Map every rank's window (handles in rank order).  wait_mode 0: spin in the sum
+        kernel when every rank has its own GPU, stream memory operations otherwise."""
+        blob = b"".join(bytes(h) for h in handles)
+        if len(blob) != PEER_HANDLE_BYTES * self.nranks:
+            raise ConfigError("peer_attach needs one handle per rank")
+        err = _Err()
+        _raise(_lib.bgs_ctx_peer_attach(self._h, ctypes.create_string_buffer(blob, len(blob)),
+                                        int(wait_mode), ctypes.byref(err)), err)
 
     def set_stream(self, stream: int) -> None:
         """cudaStream_t (as an int) whose queued work the *_device calls wait for."""

@@ -226,6 +226,26 @@ cudaError_t tsqr_cross_launch(const double* roots, int n, int s, double* ws2, do
                               int ldrout, double* mout, const DevStatus* status,
                               cudaStream_t st, int* launches);
 
+// ---------------- peer.cu: one-shot exchange over peer-mapped windows ----------------
+// Window of a rank: [flags: P x u32 in kPeerFlagBytes][parity 0: P slots][parity 1: P slots]
+constexpr int kPeerMaxRanks = 8;
+constexpr size_t kPeerFlagBytes = 256;
+struct PeerView {
+  unsigned char* win[kPeerMaxRanks];  // every rank's window as mapped here (win[rank]: local)
+  int P, rank;
+  unsigned long slot_bytes;  // bytes per (parity, source rank) slot
+};
+inline size_t peer_window_bytes(int P, size_t slot_bytes) { return kPeerFlagBytes + 2 * (size_t)P * slot_bytes; }
+// Store [a (na doubles) | b (nb doubles)] into slot (epoch & 1, rank) of every window, then
+// flag[rank] = epoch there (release, system scope).  cnt: P zeroed u32 tickets (local).
+cudaError_t peer_push_launch(const PeerView& v, const double* a, unsigned long na, const double* b,
+                             unsigned long nb, unsigned epoch, unsigned* cnt, cudaStream_t st,
+                             int* launches);
+// recv[r * ng + i] = rank r's gather part; sum[i] = the ns partials added in rank order.
+// spin: wait in the kernel for the P flags (distinct GPUs only).
+cudaError_t peer_sum_launch(const PeerView& v, unsigned long ng, double* recv, unsigned long ns,
+                            double* sum, unsigned epoch, bool spin, cudaStream_t st, int* launches);
+
 // ---------------- misc (misc.cu) ----------------
 cudaError_t gen_gaussian_launch(unsigned long long seed, long row0, long n_local, long m,
                                 double* x, long ldx, cudaStream_t st);

@@ -27,6 +27,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <unistd.h>
+
 #include <functional>
 #include <memory>
 #include <random>
@@ -148,6 +150,24 @@ PFN_encodeTiled encoder() {
   return fn;
 }
 
+// cuStreamWaitValue32 (GEQ, cyclic): the stream stalls until *addr reaches `value`; no
+// kernel occupies an SM while it waits (the peer transport's wait between launches).
+void stream_wait_geq(cudaStream_t st, unsigned* addr, unsigned value) {
+  using PFN_wait = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static PFN_wait fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      fail(BGS_E_CUDA, "cuStreamWaitValue32 unavailable");
+    fn = reinterpret_cast<PFN_wait>(p);
+  }
+  const CUresult r = fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) fail(BGS_E_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+}
+
 // The {16 rows, row block, column} 3-D view of a column-major rows x cols fp64 matrix
 // used by the tile engine (gram.cu): box {16, H, w}, 128-byte swizzle.  Reads whole
 // 16-row blocks, so the storage must hold ceil(rows/16)*16 rows per column (ld >= that).
@@ -259,7 +279,18 @@ struct bgs_ctx {
   bgs_allgather_fn hc_fn = nullptr;
   void* hc_user = nullptr;
   HBuf hc_send, hc_recv, hc_out;
-  bool collective() const { return comm != nullptr || hc_fn != nullptr; }
+  // peer-memory transport (bgs_ctx_create_peer, peer.cu): one-shot exchange over windows
+  // every rank maps (NVLink P2P between GPUs, CUDA IPC between processes)
+  struct PeerComm {
+    bool on = false, attached = false;
+    int wait_mode = 0;  // 1: stream memory operations, 2: acquire spin in the sum kernel
+    void* window = nullptr;  // cudaMalloc'ed (IPC-exportable), local
+    void* cnt = nullptr;
+    void* mapped[kPeerMaxRanks] = {};  // cudaIpcOpenMemHandle results (to close)
+    PeerView view{};
+    unsigned epoch = 0;
+  } peer;
+  bool collective() const { return comm != nullptr || hc_fn != nullptr || peer.on; }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   // The device-pointer entry points run on `stream` (non-blocking) but first wait for the
   // caller's work issued so far on `caller` (legacy default stream unless set with
@@ -349,6 +380,10 @@ struct bgs_ctx {
       event_pool.push_back(p.b);
     }
     for (auto e : event_pool) cudaEventDestroy(e);
+    for (void* mp : peer.mapped)
+      if (mp) cudaIpcCloseMemHandle(mp);
+    if (peer.window) cudaFree(peer.window);
+    if (peer.cnt) cudaFree(peer.cnt);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
     if (comm && nccl().ok) nccl().CommDestroy(comm);
@@ -646,6 +681,10 @@ class Runner {
       NCCL_OK(nccl().GroupEnd());
       return;
     }
+    if (c->peer.on) {
+      peer_exchange(send, ng, recv, sum, ns);
+      return;
+    }
     if (!c->hc_fn) fail(BGS_E_INTERNAL, "collective on a context without a communicator");
     flush_reduce();
     Prof pr(c, "host_exchange", (double)(ng + ns) * 8.0 * P, 0.0);
@@ -669,6 +708,30 @@ class Runner {
     }
     if (ng) CUDA_OK(cudaMemcpyAsync(recv, ho, (size_t)P * ng * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     if (ns) CUDA_OK(cudaMemcpyAsync(sum, ho + (size_t)P * ng, ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+
+  // The sync over peer-mapped windows (peer.cu): push to every rank, wait for the P flags
+  // (stream memory operations, or a spin in the sum kernel on distinct GPUs), sum in rank
+  // order out of the local window.  No host round trip.
+  void peer_exchange(const double* send, size_t ng, double* recv, double* sum, size_t ns) {
+    bgs_ctx::PeerComm& pc = c->peer;
+    if (!pc.attached) fail(BGS_E_COLLECTIVE, "peer context: bgs_ctx_peer_attach was not called");
+    if ((ng + ns) * sizeof(double) > pc.view.slot_bytes)
+      fail(BGS_E_CONFIG, "peer window slot (%lu bytes) is smaller than the exchange payload (%zu bytes)",
+           pc.view.slot_bytes, (ng + ns) * sizeof(double));
+    flush_reduce();
+    Prof pr(c, "peer_exchange", (double)(ng + ns) * 8.0 * P, 0.0);
+    const unsigned ep = ++pc.epoch;
+    CUDA_OK(peer_push_launch(pc.view, send, ng, sum, ns, ep, static_cast<unsigned*>(pc.cnt), c->stream,
+                             &c->launches));
+    if (pc.wait_mode == 1) {
+      for (int r = 0; r < pc.view.P; ++r) {
+        if (r == pc.view.rank) continue;  // (stream order covers the local push)
+        stream_wait_geq(c->stream, reinterpret_cast<unsigned*>(pc.window) + r, ep);
+      }
+      ++waits;
+    }
+    CUDA_OK(peer_sum_launch(pc.view, ng, recv, ns, sum, ep, pc.wait_mode == 2, c->stream, &c->launches));
   }
 
   // RecurrenceProbe::on_eval (bcgs.cpp:339-343): S2 of step k and this rank's rows of Q_k
@@ -1872,6 +1935,213 @@ int bgs_ctx_create_host_comm(int device, int rank, int nranks, bgs_allgather_fn 
   return BGS_OK;
 }
 
+// ---- peer-memory transport (peer.cu) ----
+namespace {
+// The 128-byte blob ranks exchange: the IPC handle of the window plus what attach checks.
+struct PeerBlob {
+  cudaIpcMemHandle_t ipc;  // 64 bytes
+  unsigned char uuid[16];  // the GPU (ranks on one GPU must not spin on each other)
+  int rank, nranks;
+  unsigned long slot_bytes;
+  long pid;
+  unsigned long window;  // the window's address in the exporting process (same-process attach)
+  char pad[16];
+};
+static_assert(sizeof(PeerBlob) == BGS_PEER_HANDLE_BYTES, "peer blob layout");
+}  // namespace
+
+int bgs_ctx_create_peer(int device, int rank, int nranks, unsigned long slot_bytes, bgs_ctx** out,
+                        bgs_error* err) {
+  clear_err(err);
+  *out = nullptr;
+  if (nranks < 1 || nranks > kPeerMaxRanks || rank < 0 || rank >= nranks) {
+    if (err) {
+      err->code = BGS_E_COLLECTIVE;
+      snprintf(err->msg, sizeof err->msg, "peer context: need 0 <= rank < nranks <= %d", kPeerMaxRanks);
+    }
+    return BGS_E_COLLECTIVE;
+  }
+  bgs_ctx* c = nullptr;
+  const int rc = bgs_ctx_create(device, 0, 1, nullptr, &c, err);
+  if (rc != BGS_OK) return rc;
+  try {
+    c->rank = rank;
+    c->nranks = nranks;
+    // default slot: the largest exchange validate() admits, (m + 2s) x 2s Gram + an s x s root
+    if (!slot_bytes) slot_bytes = ((4096ul + 32) * 32 + 256 + 64) * sizeof(double);
+    slot_bytes = (slot_bytes + 255) / 256 * 256;
+    const size_t wb = peer_window_bytes(nranks, slot_bytes);
+    CUDA_OK(cudaMalloc(&c->peer.window, wb));  // plain cudaMalloc: IPC-exportable
+    CUDA_OK(cudaMemset(c->peer.window, 0, wb));
+    CUDA_OK(cudaMalloc(&c->peer.cnt, 64));
+    CUDA_OK(cudaMemset(c->peer.cnt, 0, 64));
+    CUDA_OK(cudaDeviceSynchronize());
+    c->peer.on = true;
+    c->peer.view.P = nranks;
+    c->peer.view.rank = rank;
+    c->peer.view.slot_bytes = slot_bytes;
+    c->peer.view.win[rank] = static_cast<unsigned char*>(c->peer.window);
+    *out = c;
+    return BGS_OK;
+  } catch (const Fail& f) {
+    delete c;
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_ctx_peer_handle(bgs_ctx* c, void* handle, bgs_error* err) {
+  clear_err(err);
+  try {
+    if (!c || !c->peer.on) fail(BGS_E_COLLECTIVE, "not a peer context");
+    CUDA_OK(cudaSetDevice(c->device));
+    PeerBlob b;
+    memset(&b, 0, sizeof b);
+    CUDA_OK(cudaIpcGetMemHandle(&b.ipc, c->peer.window));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, c->device));
+    memcpy(b.uuid, &prop.uuid, 16);
+    b.rank = c->rank;
+    b.nranks = c->nranks;
+    b.slot_bytes = c->peer.view.slot_bytes;
+    b.pid = (long)getpid();
+    b.window = reinterpret_cast<unsigned long>(c->peer.window);
+    memcpy(handle, &b, sizeof b);
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+int bgs_ctx_peer_attach(bgs_ctx* c, const void* handles, int wait_mode, bgs_error* err) {
+  clear_err(err);
+  try {
+    if (!c || !c->peer.on) fail(BGS_E_COLLECTIVE, "not a peer context");
+    if (c->peer.attached) fail(BGS_E_COLLECTIVE, "peer context already attached");
+    if (wait_mode < 0 || wait_mode > 2) fail(BGS_E_CONFIG, "peer wait mode must be 0 (auto), 1 (stream) or 2 (spin)");
+    CUDA_OK(cudaSetDevice(c->device));
+    const int P = c->nranks;
+    const PeerBlob* hb = static_cast<const PeerBlob*>(handles);
+    bool shared_gpu = false;
+    for (int r = 0; r < P; ++r) {
+      PeerBlob b;
+      memcpy(&b, hb + r, sizeof b);
+      if (b.rank != r || b.nranks != P || b.slot_bytes != c->peer.view.slot_bytes)
+        fail(BGS_E_COLLECTIVE, "peer handle %d does not match (rank %d of %d, slot %lu bytes)", r,
+             b.rank, b.nranks, b.slot_bytes);
+      for (int t = 0; t < r; ++t)
+        if (memcmp(hb[t].uuid, b.uuid, 16) == 0) shared_gpu = true;
+      if (r == c->rank) continue;
+      if (b.pid == (long)getpid()) {
+        // a rank of this process (one process driving several contexts): its window is a
+        // plain device pointer here; on another GPU it needs peer access
+        cudaPointerAttributes at;
+        CUDA_OK(cudaPointerGetAttributes(&at, reinterpret_cast<void*>(b.window)));
+        if (at.device != c->device) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); e = cudaSuccess; }
+          CUDA_OK(e);
+        }
+        c->peer.view.win[r] = reinterpret_cast<unsigned char*>(b.window);
+      } else {
+        void* mp = nullptr;
+        CUDA_OK(cudaIpcOpenMemHandle(&mp, b.ipc, cudaIpcMemLazyEnablePeerAccess));
+        c->peer.mapped[r] = mp;
+        c->peer.view.win[r] = static_cast<unsigned char*>(mp);
+      }
+    }
+    // Ranks that share a GPU must never wait inside a kernel (nothing guarantees their
+    // kernels run at the same time): the wait is then a stream memory operation.
+    if (wait_mode == 2 && shared_gpu && P > 1)
+      fail(BGS_E_CONFIG, "peer wait mode 2 (spin) needs every rank on its own GPU");
+    c->peer.wait_mode = wait_mode ? wait_mode : (shared_gpu ? 1 : 2);
+    c->peer.attached = true;
+    return BGS_OK;
+  } catch (const Fail& f) {
+    put_err(err, f);
+    return f.code;
+  }
+}
+
+// Protocol self-test on ONE GPU without any cross-launch waiting (B200_PROFILING.md): P
+// emulated ranks in this process; every epoch all ranks push (no waits), the device is
+// synchronized, then every rank runs the SPIN flavour of the sum kernel -- its flags are
+// already there -- and the sums must equal the rank-ordered host sum bitwise on all ranks.
+int bgs_peer_selftest(int device, int nranks, long ng, long ns, int epochs, bgs_error* err) {
+  clear_err(err);
+  std::vector<bgs_ctx*> cs((size_t)std::max(nranks, 0), nullptr);
+  int rc = BGS_OK;
+  try {
+    if (nranks < 1 || nranks > kPeerMaxRanks || ng < 0 || ns < 1 || epochs < 1)
+      fail(BGS_E_CONFIG, "peer selftest: bad arguments");
+    const size_t w = (size_t)(ng + ns);
+    std::vector<PeerBlob> blobs((size_t)nranks);
+    for (int r = 0; r < nranks; ++r) {
+      bgs_error e2;
+      if (bgs_ctx_create_peer(device, r, nranks, w * sizeof(double), &cs[r], &e2) != BGS_OK)
+        fail(e2.code, "%s", e2.msg);
+      if (bgs_ctx_peer_handle(cs[r], &blobs[r], &e2) != BGS_OK) fail(e2.code, "%s", e2.msg);
+    }
+    for (int r = 0; r < nranks; ++r) {
+      bgs_error e2;
+      // mode 1 passes the shared-GPU check; the sum kernels below still spin (on flags
+      // that are already set)
+      if (bgs_ctx_peer_attach(cs[r], blobs.data(), 1, &e2) != BGS_OK) fail(e2.code, "%s", e2.msg);
+    }
+    std::vector<DBuf> gin((size_t)nranks), sin((size_t)nranks), gout((size_t)nranks);
+    std::vector<std::vector<double>> hg((size_t)nranks), hs((size_t)nranks);
+    std::mt19937_64 gen(777);
+    for (int ep = 1; ep <= epochs; ++ep) {
+      for (int r = 0; r < nranks; ++r) {
+        hg[r].resize((size_t)ng + 1);
+        hs[r].resize((size_t)ns);
+        for (auto& v : hg[r]) v = (double)(long)(gen() >> 11) * 0x1p-53 - 0.5;
+        for (auto& v : hs[r]) v = ((double)(long)(gen() >> 11) * 0x1p-53 - 0.5) * (double)(1 << (gen() % 40));
+        gin[r].ensure(((size_t)ng + 1) * 8);
+        sin[r].ensure((size_t)ns * 8);
+        gout[r].ensure(((size_t)ng * nranks + 1) * 8);
+        CUDA_OK(cudaMemcpy(gin[r].p, hg[r].data(), (size_t)ng * 8, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(sin[r].p, hs[r].data(), (size_t)ns * 8, cudaMemcpyHostToDevice));
+      }
+      for (int r = 0; r < nranks; ++r) {
+        bgs_ctx* c = cs[r];
+        c->peer.epoch = (unsigned)ep;
+        CUDA_OK(peer_push_launch(c->peer.view, gin[r].d(), (unsigned long)ng, sin[r].d(),
+                                 (unsigned long)ns, (unsigned)ep, static_cast<unsigned*>(c->peer.cnt),
+                                 c->stream, nullptr));
+      }
+      CUDA_OK(cudaDeviceSynchronize());  // every flag of this epoch is set: nothing below waits
+      for (int r = 0; r < nranks; ++r)
+        CUDA_OK(peer_sum_launch(cs[r]->peer.view, (unsigned long)ng, gout[r].d(), (unsigned long)ns,
+                                sin[r].d(), (unsigned)ep, true, cs[r]->stream, nullptr));
+      CUDA_OK(cudaDeviceSynchronize());
+      std::vector<double> want((size_t)ns), got((size_t)ns), gg((size_t)ng * nranks + 1);
+      for (long i = 0; i < ns; ++i) {
+        double acc = hs[0][(size_t)i];
+        for (int r = 1; r < nranks; ++r) acc += hs[r][(size_t)i];
+        want[(size_t)i] = acc;
+      }
+      for (int r = 0; r < nranks; ++r) {
+        CUDA_OK(cudaMemcpy(got.data(), sin[r].p, (size_t)ns * 8, cudaMemcpyDeviceToHost));
+        if (memcmp(got.data(), want.data(), (size_t)ns * 8) != 0)
+          fail(BGS_E_INTERNAL, "peer selftest: rank %d epoch %d: sum differs from the rank-ordered sum", r, ep);
+        if (ng) {
+          CUDA_OK(cudaMemcpy(gg.data(), gout[r].p, (size_t)ng * nranks * 8, cudaMemcpyDeviceToHost));
+          for (int t = 0; t < nranks; ++t)
+            if (memcmp(gg.data() + (size_t)t * ng, hg[t].data(), (size_t)ng * 8) != 0)
+              fail(BGS_E_INTERNAL, "peer selftest: rank %d epoch %d: gathered part of rank %d differs", r, ep, t);
+        }
+      }
+    }
+  } catch (const Fail& f) {
+    put_err(err, f);
+    rc = f.code;
+  }
+  for (bgs_ctx* c : cs) bgs_ctx_destroy(c);
+  return rc;
+}
+
 int bgs_ctx_set_stream(bgs_ctx* c, void* stream) {
   if (!c) return BGS_E_CUDA;
   c->caller = static_cast<cudaStream_t>(stream);
@@ -2185,7 +2455,7 @@ int bgs_factor_device_opts(bgs_ctx* c, int variant, long n, long m, long s, long
     // launches).  Not with a host communicator (its exchanges synchronize), a probe, or
     // the profilers.
     const char* eg = getenv("BGS_GRAPH");
-    const bool graphable = !(eg && *eg == '0') && !c->hc_fn && !(opts && opts->probe) &&
+    const bool graphable = !(eg && *eg == '0') && !c->hc_fn && !c->peer.on && !(opts && opts->probe) &&
                            !c->prof_on && !run.tile_prof && !run.prof_step;
     std::string key;
     if (graphable) {

@@ -65,6 +65,15 @@ def host_allgather(dist) -> Callable[[bytes], bytes]:
     return allgather
 
 
+def attach_peers(dist, ctx, wait_mode: int = 0) -> None:
+    """Exchange the window handles of a ``Context(peer=True)`` over torch.distributed and
+    map every rank's window (bgs_ctx_peer_handle / bgs_ctx_peer_attach)."""
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, ctx.peer_handle())
+    ctx.peer_attach(handles, wait_mode)
+    dist.barrier()  # every window is mapped before anyone pushes
+
+
 def gather_rows(dist, local: np.ndarray, n: int, world: int) -> np.ndarray:
     """Concatenate the ranks' row shards in rank order; every rank gets the n x m matrix
     (Communicator::gather_rows, communicator.cpp:319-336)."""

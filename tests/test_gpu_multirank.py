@@ -1,6 +1,8 @@
 """Multi-rank runs on the one GPU this pool lends: P processes share cuda:0, each with its
-own context, its own row shard and the library's host-communicator hook
-(bgs_ctx_create_host_comm) carried over torch.distributed gloo.  NCCL refuses two ranks on
+own context and its own row shard, over two transports: the library's host-communicator
+hook (bgs_ctx_create_host_comm) carried over torch.distributed gloo, and the one-shot
+exchange over peer-mapped windows (bgs_ctx_create_peer: CUDA IPC between the processes,
+stream memory operations for the wait).  NCCL refuses two ranks on
 one device, and no kernel here waits on another rank (the exchange happens between
 launches), so this is safe on a single GPU (B200_PROFILING.md: no cross-rank spinning).
 
@@ -41,7 +43,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cases, q):
+def _worker(rank, world, port, cases, q, transport="host"):
     import torch
     import torch.distributed as dist
 
@@ -52,7 +54,13 @@ def _worker(rank, world, port, cases, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         o = Oracle()
-        ctx = bgs.Context(0, rank, world, host_allgather=bd.host_allgather(dist))
+        if transport == "peer":
+            # one-shot exchange over CUDA-IPC windows; the ranks share cuda:0, so the
+            # library waits with stream memory operations (no kernel spins on a rank)
+            ctx = bgs.Context(0, rank, world, peer=True)
+            bd.attach_peers(dist, ctx)
+        else:
+            ctx = bgs.Context(0, rank, world, host_allgather=bd.host_allgather(dist))
         for ci, (v, n, m, s, P, kappa, gauss) in enumerate(cases):
             if P != world:
                 continue
@@ -77,29 +85,47 @@ def _worker(rank, world, port, cases, q):
         dist.destroy_process_group()
 
 
-def _run_world(world):
+def _run_world(world, transport="host"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     res, done = {}, 0
-    while done < world:
-        item = q.get(timeout=600)
-        if item[0] < 0:
-            done += 1
-            continue
-        res.setdefault(item[0], {})[item[1]] = item
+    try:
+        while done < world:
+            item = q.get(timeout=300)
+            if item[0] < 0:
+                done += 1
+                continue
+            res.setdefault(item[0], {})[item[1]] = item
+    finally:
+        for p in procs:  # a stuck rank must not outlive the test (exact PIDs we started)
+            p.join(timeout=60 if done == world else 1)
+            if p.is_alive():
+                p.kill()
+                p.join(timeout=10)
     for p in procs:
-        p.join(timeout=120)
         assert p.exitcode == 0
     return res
 
 
+@pytest.mark.parametrize("n_ranks,ng,ns", [(2, 16, 3000), (4, 0, 1), (8, 256, 26000), (3, 9, 100000)])
+def test_peer_exchange_protocol_selftest(n_ranks, ng, ns):
+    """The one-shot peer exchange (peer.cu) with emulated ranks in one process: every
+    epoch all ranks push into all windows, then the spin flavour of the sum kernel runs
+    with its flags already set.  Checked bitwise against the rank-ordered host sum on every
+    rank, over both parities (bgs_peer_selftest)."""
+    import paper_2507_21791_b200 as bgs
+    bgs.peer_selftest(0, n_ranks, ng, ns, 6)
+
+
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_ranks_sharing_one_gpu_match_oracle(oracle, world):
-    res = _run_world(world)
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_ranks_sharing_one_gpu_match_oracle(oracle, world, transport):
+    res = _run_world(world, transport)
     mine = [ci for ci, c in enumerate(CASES) if c[4] == world]
     assert sorted(res) == mine
     for ci in mine:

@@ -10,5 +10,5 @@ nvcc $F -c csrc/small.cu -o _build/small_st.o &
 nvcc $F -c csrc/k12.cu -o _build/k12_st.o
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o _lib_exp/st.so _build/gram.o _build/gram_ct.o \
-  _build/k12_st.o _build/k12_ct.o _build/update.o _build/update_tma.o _build/small_st.o _build/tsqr.o _build/misc.o \
+  _build/k12_st.o _build/k12_ct.o _build/update.o _build/update_tma.o _build/small_st.o _build/tsqr.o _build/misc.o _build/peer.o \
   _build/runtime.o _build/matgen_host.o -ldl
