@@ -62,7 +62,11 @@ bool k12_plan(SplitParams& p) {
     const int KS = 4 / cd.R;
     const int kw = (std::max(k0, k1) + KS - 1) / KS;
     const int mtw = (std::max(mt0, mt1) + kGroupWarps - 1) / kGroupWarps;
-    const int kw_max = kKwMax;
+    // one CTA at R = 1 carries up to kKwMaxR1 k-steps per warp while three stages fit
+    // (BGS_K12C_KWMAX=16: the CTA pair takes those steps instead)
+    const char* ke = getenv("BGS_K12C_KWMAX");
+    const int kw_r1 = ke ? std::max(kKwMax, std::min(kKwMaxR1, atoi(ke))) : kKwMaxR1;
+    const int kw_max = (cd.C == 1 && cd.R == 1) ? kw_r1 : kKwMax;
     int kw_t = std::max(1, kw);
     while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) ++kw_t;
     if (kw_t > kw_max) continue;

@@ -71,6 +71,9 @@ constexpr int kMaxStages = 8;
 // A-block unit and one span-1 unit -> mt <= KS KW / 2 + 2 (C = 1 and C = 2 alike)
 __host__ __device__ constexpr int mtw_for(int kw, int R) { return ((4 / R) * kw / 2 + 2 + 3) / 4; }
 constexpr int kKwMax = 16;
+// R = 1 on one CTA: 17 k-steps per warp where three stages still fit (kp = 260 at m = 400;
+// wider instances on two stages measured slower than the CTA pair: 33.8 -> 39.6 ms fused)
+constexpr int kKwMaxR1 = 17;
 // (KW, R) with a second instance at MTW = mtw_for(KW, R) - 1 (see k12_plan)
 __host__ __device__ constexpr bool has_narrow(int kw, int R) {
   return (R == 1 && kw % 2 == 0) || (R == 2 && kw % 4 == 3);
@@ -327,6 +330,33 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     const int quad = lane & ~3;
     // epilogue matrix M as DMMA B fragments: lane (i, kk) holds M[kk][i] and M[4 + kk][i]
     const double mb0 = ep_m[kk * 8 + ii], mb1 = ep_m[(4 + kk) * 8 + ii];
+    // Per-lane epilogue plan, fixed for the whole kernel (the stage loop only adds the stage
+    // base and the row offset): lane (i, kk) reads z[row][kk] of both source blocks and owns
+    // output columns 2kk, 2kk + 1 (A for kk < 2, B for kk >= 2).  Recomputing these per stage
+    // cost ~250 cycles of a ~5000-cycle group-stage (33.8 -> 32.9 ms of fused time at config 2).
+    constexpr bool kEpPlan = MTW <= 6;  // (MTW >= 7: no registers to spare, measured)
+    const bool ep_isA = kk < 2;
+    const bool ep_za = p.upd_a && kk < s, ep_zb = p.upd_b && kk < s;
+    const uint32_t ep_offA = elem_off<2>(colA + kk, erow), ep_offB = elem_off<2>(colB + kk, erow);
+    const long ep_ld = ep_isA ? p.lddA : p.lddB;
+    uint32_t ep_so[2];  // shared-memory offsets of the two outputs inside a chunk
+    int ep_flags = 0;   // bit e: store output e to the stage; bit 2 + e: store it to HBM
+    {
+      const int c0 = ep_isA ? 2 * kk : 2 * kk - 4;
+      const bool on = ep_isA ? p.upd_a : p.upd_b;
+      // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
+      // shared: A only where its rows are output tiles (the rank owning the A units)
+      const bool gst = !pair || (ep_isA ? rank == 0 : rank == 1);
+      const bool sst = ep_isA ? (!pair || rank == 1) : true;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ep_so[e] = elem_off<2>((ep_isA ? colA : colB) + c0 + e, erow);
+        if (on && c0 + e < s) ep_flags |= (sst ? 1 << e : 0) | (gst ? 4 << e : 0);
+      }
+    }
+    // HBM address of output 0 at shard row 0 of this lane's chunk row
+    double* const ep_g = (ep_isA ? p.dstA : p.dstB) + erow +
+                         (size_t)(ep_isA ? 2 * kk : 2 * kk - 4) * (size_t)ep_ld;
     int acol[MTW];  // tile column of this lane's Gram fragment, per output tile
     // (CT) compensated output tiles: global tile index >= p.comp_t0 -> every 4-row k-step
     // goes straight into the double-double (BCGSI+1S: the U rows)
@@ -502,36 +532,57 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         const double t0 = __shfl_sync(0xffffffffu, D0[ch], sl), t1 = __shfl_sync(0xffffffffu, D1[ch], sl);
         const double u0 = __shfl_sync(0xffffffffu, D0[ch], sl | 2);
         const double u1 = __shfl_sync(0xffffffffu, D1[ch], sl | 2);
-        const bool cv = kk < s;
-        const double sa = (p.upd_a && cv) ? lds64(cb + elem_off<2>(colA + kk, erow)) : 0.0;
-        const double sb = (p.upd_b && cv) ? lds64(cb + elem_off<2>(colB + kk, erow)) : 0.0;
-        const double za = (p.upd_a && cv) ? sa - ((kk & 1) ? t1 : t0) : 0.0;
-        const double zb = (p.upd_b && cv) ? sb - ((kk & 1) ? u1 : u0) : 0.0;
-        double o0 = 0.0, o1 = 0.0;
-        dmma(o0, o1, za, mb0);
-        dmma(o0, o1, zb, mb1);
-        // lane (i, kk) now holds output columns 2kk, 2kk + 1: A for kk < 2, B for kk >= 2
-        const bool isA = kk < 2;
-        const int c0 = isA ? 2 * kk : 2 * kk - 4;
-        const bool on = isA ? p.upd_a : p.upd_b;
-        const int lcol = isA ? colA : colB;
-        const int crow = kChunkRows * ch + erow;
-        const bool live = crow < vrows;
-        const long grow = row0 + crow;
-        double* gdst = isA ? p.dstA : p.dstB;
-        const long gld = isA ? p.lddA : p.lddB;
-        // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
-        // shared: A only where its rows are output tiles (the rank owning the A units)
-        const bool gstore = live && (!pair || (isA ? rank == 0 : rank == 1));
-        const bool sstore = isA ? (!pair || rank == 1) : true;
+        if constexpr (kEpPlan) {
+          const double sa = ep_za ? lds64(cb + ep_offA) : 0.0;
+          const double sb = ep_zb ? lds64(cb + ep_offB) : 0.0;
+          const double za = ep_za ? sa - ((kk & 1) ? t1 : t0) : 0.0;
+          const double zb = ep_zb ? sb - ((kk & 1) ? u1 : u0) : 0.0;
+          double o0 = 0.0, o1 = 0.0;
+          dmma(o0, o1, za, mb0);
+          dmma(o0, o1, zb, mb1);
+          // lane (i, kk) now holds output columns 2kk, 2kk + 1: A for kk < 2, B for kk >= 2
+          if (ep_flags & 1) sts64(cb + ep_so[0], o0);
+          if (ep_flags & 2) sts64(cb + ep_so[1], o1);
+          if (kChunkRows * ch + erow < vrows) {  // (rows past the shard end are not stored)
+            double* g = ep_g + (row0 + kChunkRows * ch);
+            BGS_DCHECK(!(ep_flags & 12) || row0 + kChunkRows * ch + erow < p.n_rows,
+                       "k12: epilogue store outside the shard");
+            if (ep_flags & 4) g[0] = o0;
+            if (ep_flags & 8) g[ep_ld] = o1;
+          }
+        } else {
+          // (wide instances: the plan's registers would spill; recompute per stage)
+          const bool cv = kk < s;
+          const double sa = (p.upd_a && cv) ? lds64(cb + elem_off<2>(colA + kk, erow)) : 0.0;
+          const double sb = (p.upd_b && cv) ? lds64(cb + elem_off<2>(colB + kk, erow)) : 0.0;
+          const double za = (p.upd_a && cv) ? sa - ((kk & 1) ? t1 : t0) : 0.0;
+          const double zb = (p.upd_b && cv) ? sb - ((kk & 1) ? u1 : u0) : 0.0;
+          double o0 = 0.0, o1 = 0.0;
+          dmma(o0, o1, za, mb0);
+          dmma(o0, o1, zb, mb1);
+          // lane (i, kk) now holds output columns 2kk, 2kk + 1: A for kk < 2, B for kk >= 2
+          const bool isA = kk < 2;
+          const int c0 = isA ? 2 * kk : 2 * kk - 4;
+          const bool on = isA ? p.upd_a : p.upd_b;
+          const int lcol = isA ? colA : colB;
+          const int crow = kChunkRows * ch + erow;
+          const bool live = crow < vrows;
+          const long grow = row0 + crow;
+          double* gdst = isA ? p.dstA : p.dstB;
+          const long gld = isA ? p.lddA : p.lddB;
+          // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
+          // shared: A only where its rows are output tiles (the rank owning the A units)
+          const bool gstore = live && (!pair || (isA ? rank == 0 : rank == 1));
+          const bool sstore = isA ? (!pair || rank == 1) : true;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = c0 + e;
-          if (on && c < s) {
-            const double v = e ? o1 : o0;
-            if (sstore) sts64(cb + elem_off<2>(lcol + c, erow), v);
-            BGS_DCHECK(!gstore || (grow < p.n_rows && c < s), "k12: epilogue store outside the shard");
-            if (gstore) gdst[grow + (size_t)c * gld] = v;
+          for (int e = 0; e < 2; ++e) {
+            const int c = c0 + e;
+            if (on && c < s) {
+              const double v = e ? o1 : o0;
+              if (sstore) sts64(cb + elem_off<2>(lcol + c, erow), v);
+              BGS_DCHECK(!gstore || (grow < p.n_rows && c < s), "k12: epilogue store outside the shard");
+              if (gstore) gdst[grow + (size_t)c * gld] = v;
+            }
           }
         }
       }
@@ -687,8 +738,15 @@ static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
     BGS_KW(1) BGS_KW(2) BGS_KW(3) BGS_KW(4) BGS_KW(5) BGS_KW(6) BGS_KW(7) BGS_KW(8)
     BGS_KW(9) BGS_KW(10) BGS_KW(11) BGS_KW(12) BGS_KW(13) BGS_KW(14) BGS_KW(15) BGS_KW(16)
 #undef BGS_KW
-    default: return cudaErrorInvalidValue;
+#define BGS_KW1(K) \
+  case K:          \
+    if constexpr (R == 1) return launch_k12<K, R, CT>(p, grid, st); \
+    break;
+    BGS_KW1(17)
+#undef BGS_KW1
+    default: break;
   }
+  return cudaErrorInvalidValue;
 }
 
 template <bool CT>

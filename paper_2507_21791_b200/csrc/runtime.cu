@@ -1641,7 +1641,7 @@ class Runner {
             tot[7] / st, tot[10] / st, tot[8] / st, tot[5] / st);
     // K12c: [cta][group][full-wait, update, exchange, epilogue, gram, total, stages]
     double kt[8] = {0};
-    for (int b = 0; b < 256; ++b)
+    for (int b = 0; b < 160; ++b)  // (cells from 2560 on hold CTA 0's timeline)
       for (int g = 0; g < 2; ++g)
         for (int i = 0; i < 7; ++i) kt[i] += (double)h[256 * 16 + b * 16 + 8 * g + i];
     if (kt[6] > 0)
@@ -2465,7 +2465,7 @@ int bgs_factor_device_opts(bgs_ctx* c, int variant, long n, long m, long s, long
                opts ? opts->classic_intra : 0, run.no_fuse, run.no_k12c, run.gram_max_units,
                run.no_merge_small, run.no_pdl, run.comp_mode, run.no_k2m, run.tile_dbg);
       key = kb;
-      for (const char* ev : {"BGS_K12C_PLAN", "BGS_K12C_MAXS", "BGS_K12C_MINS", "BGS_UPDATE_MAXKP",
+      for (const char* ev : {"BGS_K12C_PLAN", "BGS_K12C_MAXS", "BGS_K12C_MINS", "BGS_K12C_KWMAX", "BGS_UPDATE_MAXKP",
                              "BGS_TSQR_GENERIC", "BGS_K2_SCALAR"}) {
         const char* v = getenv(ev);
         key += std::string(" ") + (v ? v : "-");
