@@ -183,6 +183,17 @@ BGS_DEV void sts64(uint32_t addr, double v) {
 }
 
 // ---------------------------------------------------------------------------------
+// System-scope release store / acquire load (flags of the peer-memory exchange, peer.cu)
+BGS_DEV void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+BGS_DEV unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ---------------------------------------------------------------------------------
 // Error-free transformation: a + b = s + e exactly (Knuth TwoSum).
 // ---------------------------------------------------------------------------------
 BGS_DEV void two_sum(double a, double b, double& s, double& e) {

@@ -246,6 +246,22 @@ cudaError_t peer_push_launch(const PeerView& v, const double* a, unsigned long n
 cudaError_t peer_sum_launch(const PeerView& v, unsigned long ng, double* recv, unsigned long ns,
                             double* sum, unsigned epoch, bool spin, cudaStream_t st, int* launches);
 
+// The one-sync step fused with the exchange (small.cu): A = reduce + push + flags, B =
+// [spin] + rank-ordered sum + step, AB = both in one launch (in-kernel spin).
+struct ReduceArgs;
+struct ReducePush;
+struct SmallParams;
+cudaError_t reduce_push_launch(const ReduceArgs& r, int entries, const ReducePush& push,
+                               const PeerView& v, unsigned epoch, unsigned* ticket, int sms,
+                               cudaStream_t st, int* launches);
+cudaError_t sum_small_launch(const PeerView& v, unsigned epoch, bool spin, unsigned long words,
+                             double* G, const SmallParams& p, unsigned* ticket, int sms,
+                             cudaStream_t st, int* launches);
+cudaError_t reduce_xchg_small_launch(const ReduceArgs& r, int entries, const ReducePush& push,
+                                     const PeerView& v, unsigned epoch, unsigned long words,
+                                     double* G, const SmallParams& p, unsigned* ticket, int sms,
+                                     cudaStream_t st, int* launches);
+
 // ---------------- misc (misc.cu) ----------------
 cudaError_t gen_gaussian_launch(unsigned long long seed, long row0, long n_local, long m,
                                 double* x, long ldx, cudaStream_t st);

@@ -29,15 +29,6 @@ namespace bgs {
 
 namespace {
 
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // grid (P, B): blocks (p, *) push this rank's payload into window p; the last of them to
 // finish (ticket cnt[p]) publishes flag[rank] = epoch there.
 __global__ void __launch_bounds__(512) peer_push_kernel(const PeerView v, const double* __restrict__ a,

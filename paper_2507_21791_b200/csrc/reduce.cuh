@@ -13,6 +13,13 @@ namespace bgs {
 constexpr int RED_ENTRIES = 16, RED_SLICES = 16, RED_BATCH = 8;
 constexpr int RED_THREADS = RED_ENTRIES * RED_SLICES;
 
+// Extra destinations of the reduced Gram (the one-shot exchange's windows, peer.cu): the
+// entry written to out[i] also goes to dst[0..n-1][i].
+struct ReducePush {
+  double* dst[8];
+  int n;
+};
+
 struct ReduceArgs {
   const double2* part;  // (hi, lo) partial slots
   int G;                // slots
@@ -26,7 +33,8 @@ struct ReduceArgs {
 // returns (the block barrier inside is reached by all of them).  A CTA may run several
 // entry blocks in a row: the barrier at entry protects the shared slice sums of the
 // previous one.
-BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b) {
+template <bool PUSH = false>
+BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b, const ReducePush* push = nullptr) {
   __shared__ double2 red[RED_SLICES][RED_ENTRIES];
   const int le = threadIdx.x % RED_ENTRIES, sl = threadIdx.x / RED_ENTRIES;
   const int idx = b * RED_ENTRIES + le;
@@ -77,7 +85,13 @@ BGS_DEV void gram_reduce_body(const ReduceArgs& a, int b) {
     row = a.lcols0 + r;
   }
   BGS_DCHECK(row < a.M && n < a.N, "gram_reduce: output entry outside the Gram");
-  a.out[row + (size_t)n * a.M] = s + e;
+  const double val = s + e;
+  if (PUSH) {
+#pragma unroll 1
+    for (int d = 0; d < push->n; ++d) push->dst[d][row + (size_t)n * a.M] = val;
+  } else {
+    a.out[row + (size_t)n * a.M] = val;
+  }
 }
 
 }  // namespace bgs

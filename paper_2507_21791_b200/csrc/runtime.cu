@@ -511,6 +511,10 @@ class Runner {
     no_k2m = ek2m && *ek2m == '0';
     const char* ect = getenv("BGS_COMP_TAIL");
     comp_mode = !ect ? 1 : (*ect == '0' ? 0 : (strcmp(ect, "all") == 0 ? 2 : 1));
+    const char* e7 = getenv("BGS_NO_PEER_FUSE");
+    no_peer_fuse = e7 && *e7 && *e7 != '0';
+    const char* e8 = getenv("BGS_PEER_ONE");
+    peer_one = e8 ? atoi(e8) : 1;
     const char* e6 = getenv("BGS_NO_PDL");
     no_pdl = e6 && *e6 && *e6 != '0';
     const char* d = getenv("BGS_TILE_DBG");
@@ -859,7 +863,7 @@ class Runner {
     rp.lcols[1] = lc[1];
     rp.status = status;
     reduce(rp, slot_base, c->G.d(), 0, (double)slot_base * per_slot * 8.0);
-    if (use_coll && do_allreduce) allreduce(c->G.d(), (size_t)M * p.N);
+    if (use_coll && do_allreduce) allreduce_after_reduce(c->G.d(), (size_t)M * p.N);
     if (count_sync) record(label, (long)M * p.N);
     return M;
   }
@@ -867,23 +871,48 @@ class Runner {
   // A Gram reduction held back so the one-sync step's small op can run in the same launch
   // (reduce_step4_kernel).  Only inside onesync(), only on single-GPU contexts (no
   // allreduce may sit between the two); every other launch flushes it first.
+  // On a peer-memory context (peer.cu) the cross-rank exchange of that Gram is held back
+  // with it (xchg): reduce -> push -> flags and [wait] -> rank-ordered sum -> step then run
+  // as two launches, or one (small.cu: reduce_push / sum_step4 / reduce_xchg_step4).
   struct PendingReduce {
     bool on = false;
     ReduceArgs a;
     int entries = 0;
     double bytes = 0.0;
+    bool xchg = false;   // an allreduce of `words` doubles at a.out follows the reduction
+    size_t words = 0;
   };
   PendingReduce pend;
   bool defer_reduce = false;
+  bool no_peer_fuse = false;  // BGS_NO_PEER_FUSE: separate reduce / push / sum / step launches
+  int peer_one = 1;           // BGS_PEER_ONE=0: never the single-launch form (A then B)
+  bool peer_fusable() const {
+    return c->peer.on && c->peer.attached && !no_peer_fuse && !c->comm && !c->hc_fn;
+  }
   void flush_reduce() {
     if (!pend.on) return;
     pend.on = false;
-    Prof pr(c, "gram_reduce", pend.bytes, 0.0);
-    CUDA_OK(gram_reduce_launch_args(pend.a, pend.entries, c->stream, &c->launches));
+    {
+      Prof pr(c, "gram_reduce", pend.bytes, 0.0);
+      CUDA_OK(gram_reduce_launch_args(pend.a, pend.entries, c->stream, &c->launches));
+    }
+    if (pend.xchg) {
+      pend.xchg = false;
+      allreduce(pend.a.out, pend.words);
+    }
+  }
+  // the allreduce that follows a reduction into d: rides with a held-back reduction
+  void allreduce_after_reduce(double* d, size_t n) {
+    if (pend.on && pend.a.out == d) {
+      pend.xchg = true;
+      pend.words = n;
+      return;
+    }
+    allreduce(d, n);
   }
   // launch (or hold back) the reduction of `slots` partial slots described by rp
   void reduce(const TileParams& rp, int slots, double* out, int ld_out, double bytes) {
-    if (defer_reduce && !use_coll && !gout) {
+    if (defer_reduce && (!use_coll || peer_fusable()) && !gout) {
       pend.on = true;
       pend.a = reduce_args(rp, slots, out, ld_out);
       pend.entries = rp.mt_out * 8 * 8 * gram_n_tiles(rp.N);
@@ -1062,7 +1091,7 @@ class Runner {
     }
     p.partial = c->partial.d();
     reduce(p, cta_base, gout ? gout : c->G.d(), gout ? gout_ld : 0, (double)cta_base * per_cta * 8.0);
-    if (use_coll && do_allreduce) allreduce(c->G.d(), (size_t)M * p.N);
+    if (use_coll && do_allreduce) allreduce_after_reduce(c->G.d(), (size_t)M * p.N);
     if (count_sync) record(label, (long)M * p.N);
     return M;
   }
@@ -1183,7 +1212,49 @@ class Runner {
     p.R = c->R.d();
     p.ldr = (int)m;
     p.status = status;
-    if (pend.on && small_mergeable(p)) {
+    if (pend.on && pend.xchg && small_mergeable(p)) {
+      // the step across ranks: reduce + push + flags, [wait], rank-ordered sum + step
+      bgs_ctx::PeerComm& pc = c->peer;
+      if (pend.words * sizeof(double) > pc.view.slot_bytes)
+        fail(BGS_E_CONFIG, "peer window slot (%lu bytes) is smaller than the exchange payload (%zu bytes)",
+             pc.view.slot_bytes, pend.words * sizeof(double));
+      pend.on = false;
+      pend.xchg = false;
+      const unsigned ep = ++pc.epoch;
+      ReducePush push;
+      memset(&push, 0, sizeof push);
+      push.n = pc.view.P;
+      for (int r = 0; r < pc.view.P; ++r)
+        push.dst[r] = reinterpret_cast<double*>(
+            pc.view.win[r] + kPeerFlagBytes +
+            ((size_t)(ep & 1u) * pc.view.P + pc.view.rank) * pc.view.slot_bytes);
+      unsigned* tk = static_cast<unsigned*>(c->ticket.p);
+      if (pc.wait_mode == 2 && peer_one) {
+        Prof pr(c, "reduce_xchg_small", pend.bytes, 0.0);
+        CUDA_OK(reduce_xchg_small_launch(pend.a, pend.entries, push, pc.view, ep, pend.words,
+                                         pend.a.out, p, tk, c->sms, c->stream, &c->launches));
+      } else {
+        {
+          Prof pr(c, "reduce_push", pend.bytes, 0.0);
+          CUDA_OK(reduce_push_launch(pend.a, pend.entries, push, pc.view, ep, tk, c->sms, c->stream,
+                                     &c->launches));
+        }
+        if (pc.wait_mode == 1) {
+          for (int r = 0; r < pc.view.P; ++r) {
+            if (r == pc.view.rank) continue;  // (stream order covers the local push)
+            stream_wait_geq(c->stream, reinterpret_cast<unsigned*>(pc.window) + r, ep);
+          }
+          ++waits;
+        }
+        Prof pr(c, "sum_small", (double)pend.words * 8.0 * pc.view.P, 0.0);
+        CUDA_OK(sum_small_launch(pc.view, ep, pc.wait_mode == 2, pend.words, pend.a.out, p, tk,
+                                 c->sms, c->stream, &c->launches));
+      }
+      merged_mark = c->launches;
+      merged_waits = waits;
+      return;
+    }
+    if (pend.on && !pend.xchg && small_mergeable(p)) {
       pend.on = false;
       Prof pr(c, "reduce_small", pend.bytes, 0.0);
       CUDA_OK(reduce_small_launch(pend.a, pend.entries, p, static_cast<unsigned*>(c->ticket.p),

@@ -794,6 +794,93 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   onesync_step4_body(p);
 }
 
+// ---------------------------------------------------------------------------------------
+// The one-sync step across ranks over peer-mapped windows (peer.cu), fused with its
+// neighbours: SURVEY.md 8(f) row 4, replacing exact_allreduce (communicator.cpp:226-250)
+// between fused_gram and the step's small operations.
+//   A  reduce_push_kernel: every CTA reduces its slice of the local Gram partials and
+//      stores the entries straight into slot (epoch & 1, rank) of EVERY rank's window
+//      (NVLink / NVSwitch peer stores); the last CTA publishes flag[rank] = epoch
+//      everywhere (release, system scope).
+//   B  sum_step4_kernel: [acquire-spin on the P local flags: distinct GPUs only; ranks that
+//      share a GPU wait with stream memory operations before the launch] every CTA adds
+//      its slice of the P partials in rank order into G (same order on every rank ->
+//      bitwise replicated); the last CTA runs the step.  Triggers the programmatic launch
+//      of the next fused kernel at entry, like the single-GPU merged kernel.
+//   AB reduce_xchg_step4_kernel: A and B in ONE launch (in-kernel spin; distinct GPUs).
+// A block step is then fused kernel -> A -> B (or AB) -> fused kernel instead of fused ->
+// gram_reduce -> push -> sum -> step -> fused.
+BGS_DEV void peer_sum_body(const PeerView& v, unsigned epoch, int spin, unsigned long words,
+                           double* __restrict__ G) {
+  unsigned char* win = v.win[v.rank];
+  if (spin) {
+    if ((int)threadIdx.x < v.P) {
+      const unsigned* f = reinterpret_cast<const unsigned*>(win) + threadIdx.x;
+      while ((int)(ld_acquire_sys(f) - epoch) < 0) __nanosleep(20);
+    }
+    __syncthreads();
+  }
+  const double* base = reinterpret_cast<const double*>(win + kPeerFlagBytes +
+                                                       (size_t)(epoch & 1u) * v.P * v.slot_bytes);
+  const unsigned long sd = v.slot_bytes / sizeof(double);
+  const unsigned long stride = (unsigned long)gridDim.x * blockDim.x;
+  for (unsigned long i = (unsigned long)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride) {
+    double acc = __ldcv(base + i);
+    for (int r = 1; r < v.P; ++r) acc += __ldcv(base + (size_t)r * sd + i);  // rank order
+    G[i] = acc;
+  }
+}
+
+// true in exactly one CTA: the last one to get here (re-arms the ticket)
+BGS_DEV bool last_cta(unsigned* ticket, bool system_scope) {
+  __shared__ int last;
+  if (system_scope) __threadfence_system(); else __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return false;
+  if (system_scope) __threadfence_system(); else __threadfence();
+  if (threadIdx.x == 0) *ticket = 0u;
+  return true;
+}
+
+BGS_DEV void publish_flags(const PeerView& v, unsigned epoch) {
+  if ((int)threadIdx.x < v.P)
+    st_release_sys(reinterpret_cast<unsigned*>(v.win[threadIdx.x]) + v.rank, epoch);
+}
+
+__global__ void __launch_bounds__(kStepThreads, 1)
+    reduce_push_kernel(const ReduceArgs r, int nblk, const ReducePush push, const PeerView v,
+                       unsigned epoch, unsigned* ticket) {
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) gram_reduce_body<true>(r, b, &push);
+  if (!last_cta(ticket, true)) return;
+  publish_flags(v, epoch);
+}
+
+__global__ void __launch_bounds__(kStepThreads, 1)
+    sum_step4_kernel(const PeerView v, unsigned epoch, int spin, unsigned long words, double* G,
+                     SmallParams p, unsigned* ticket) {
+  griddep_launch_dependents();
+  peer_sum_body(v, epoch, spin, words, G);
+  if (!last_cta(ticket, false)) return;
+  onesync_step4_body(p);
+}
+
+__global__ void __launch_bounds__(kStepThreads, 1)
+    reduce_xchg_step4_kernel(const ReduceArgs r, int nblk, const ReducePush push, const PeerView v,
+                             unsigned epoch, unsigned long words, double* G, SmallParams p,
+                             unsigned* ticket) {
+  griddep_launch_dependents();
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) gram_reduce_body<true>(r, b, &push);
+  if (last_cta(ticket, true)) publish_flags(v, epoch);
+  // (every CTA of this grid is resident -- one wave -- so the spin cannot starve the CTA
+  // that publishes this rank's flag; the peers' flags arrive over NVLink)
+  __syncthreads();
+  peer_sum_body(v, epoch, 1, words, G);
+  if (!last_cta(ticket + 1, false)) return;
+  onesync_step4_body(p);
+}
+
 bool small_mergeable(const SmallParams& p) {
   return p.mode == SM_ONESYNC_STEP && p.s <= 4 && p.kp <= 2 * kStepThreads && !p.sdiag_prev_copy;
 }
@@ -805,6 +892,38 @@ cudaError_t reduce_small_launch(const ReduceArgs& r, int entries, const SmallPar
   // are looped over inside the CTA instead of running as a second wave
   const int nblk = (entries + RED_ENTRIES - 1) / RED_ENTRIES;
   reduce_step4_kernel<<<std::min(nblk, sms), kStepThreads, 0, st>>>(r, nblk, p, ticket);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_push_launch(const ReduceArgs& r, int entries, const ReducePush& push,
+                               const PeerView& v, unsigned epoch, unsigned* ticket, int sms,
+                               cudaStream_t st, int* launches) {
+  const int nblk = (entries + RED_ENTRIES - 1) / RED_ENTRIES;
+  reduce_push_kernel<<<std::min(nblk, sms), kStepThreads, 0, st>>>(r, nblk, push, v, epoch, ticket);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t sum_small_launch(const PeerView& v, unsigned epoch, bool spin, unsigned long words,
+                             double* G, const SmallParams& p, unsigned* ticket, int sms,
+                             cudaStream_t st, int* launches) {
+  if (!small_mergeable(p)) return cudaErrorInvalidValue;
+  const int grid = (int)std::max<unsigned long>(1, std::min<unsigned long>(sms, (words + kStepThreads - 1) / kStepThreads));
+  sum_step4_kernel<<<grid, kStepThreads, 0, st>>>(v, epoch, spin ? 1 : 0, words, G, p, ticket);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_xchg_small_launch(const ReduceArgs& r, int entries, const ReducePush& push,
+                                     const PeerView& v, unsigned epoch, unsigned long words,
+                                     double* G, const SmallParams& p, unsigned* ticket, int sms,
+                                     cudaStream_t st, int* launches) {
+  if (!small_mergeable(p)) return cudaErrorInvalidValue;
+  const int nblk = (entries + RED_ENTRIES - 1) / RED_ENTRIES;
+  // one wave (<= one CTA per SM: the step body's registers allow no more), see the kernel
+  reduce_xchg_step4_kernel<<<std::min(nblk, sms), kStepThreads, 0, st>>>(r, nblk, push, v, epoch,
+                                                                       words, G, p, ticket);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

@@ -43,7 +43,8 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cases, q, transport="host"):
+def _worker(rank, world, port, cases, q, transport="host", env=None):
+    os.environ.update(env or {})  # (runtime switches are read per call / per Runner)
     import torch
     import torch.distributed as dist
 
@@ -85,11 +86,11 @@ def _worker(rank, world, port, cases, q, transport="host"):
         dist.destroy_process_group()
 
 
-def _run_world(world, transport="host"):
+def _run_world(world, transport="host", env=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q, transport))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q, transport, env))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -165,3 +166,60 @@ def test_multirank_matches_emulated_procs(oracle):
         r = res[ci][0][3]
         assert np.abs(r - emu.r).max() <= 1e-12 * np.abs(emu.r).max()
         assert emu.stats.sync_count == res[ci][0][5]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_fused_step_equals_separate_launches(world):
+    """The one-sync step over the peer windows as two launches (reduce + push + flags, then
+    rank-ordered sum + step: small.cu) against the same exchange as separate reduce / push /
+    sum / step launches (BGS_NO_PEER_FUSE=1): same bits in R and Q on every rank, same
+    sync accounting."""
+    fused = _run_world(world, "peer")
+    plain = _run_world(world, "peer", {"BGS_NO_PEER_FUSE": "1"})
+    mine = [ci for ci, c in enumerate(CASES) if c[4] == world]
+    assert sorted(fused) == mine and sorted(plain) == mine
+    for ci in mine:
+        for rk in range(world):
+            a, b = fused[ci][rk], plain[ci][rk]
+            assert a[2] == "ok" and b[2] == "ok", (CASES[ci], a[2], b[2])
+            assert np.array_equal(a[3].view(np.int64), b[3].view(np.int64)), CASES[ci]
+            assert np.array_equal(a[4].view(np.int64), b[4].view(np.int64)), CASES[ci]
+            assert a[5:] == b[5:]
+
+
+@pytest.mark.parametrize("one_launch", [1, 0])
+@pytest.mark.parametrize("variant", [3, 5])
+def test_peer_step_with_in_kernel_wait_on_one_rank(oracle, variant, one_launch, monkeypatch):
+    """A one-rank peer context in the distinct-GPU mode (wait_mode 2: the flags are awaited
+    inside the kernel).  one_launch = 1: reduce + push + flags + spin + sum + step in ONE
+    kernel (reduce_xchg_step4_kernel); 0: two kernels, the second spinning at its head.
+    With one rank the exchange is an identity, so R and Q must have the bits of the local
+    (no-communicator) path, with fewer launches than the separate-launch exchange."""
+    import torch
+
+    import paper_2507_21791_b200 as bgs
+    monkeypatch.setenv("BGS_PEER_ONE", str(one_launch))
+    n, m, s = 20000, 64, 4
+    x = oracle.gen_matrix(n, m, s, 1e4, 777, False)
+    ld = (n + 31) // 32 * 32
+
+    def run(ctx):
+        X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+        X[:, :n] = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        Q = torch.zeros_like(X)
+        r, st, tm = bgs.factor_device(ctx, variant, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+        return r, Q[:, :n].cpu().numpy(), st, tm
+
+    local = run(bgs.Context(0))
+    pctx = bgs.Context(0, 0, 1, peer=True)
+    pctx.peer_attach([pctx.peer_handle()], 2)
+    fused = run(pctx)
+    monkeypatch.setenv("BGS_NO_PEER_FUSE", "1")
+    plain = run(pctx)
+    for other in (fused, plain):
+        assert np.array_equal(local[0].view(np.int64), other[0].view(np.int64))
+        assert np.array_equal(local[1].view(np.int64), other[1].view(np.int64))
+        assert local[2].sync_count == other[2].sync_count
+    steps = m // s - 2
+    # separate launches: reduce, push, sum, step per block step; fused: 1 or 2
+    assert plain[3].kernel_launches - fused[3].kernel_launches >= steps * (3 if one_launch else 2) - 4
