@@ -45,6 +45,11 @@ def parse():
                          "workload), 5 (n=1e7 m=400 geometric kappa=1e6)")
     ap.add_argument("--nccl", action="store_true",
                     help="N=1: run the collective path on a one-rank NCCL communicator")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: the per-step exchange over NCCL (default) or the library's one-shot "
+                         "exchange over peer-mapped windows fused with the step kernel (NVLink P2P "
+                         "stores, in-kernel wait; bgs_ctx_create_peer); N=1 with 'peer': a one-rank "
+                         "peer context")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -81,7 +86,9 @@ def workload_config(a, world):
         "variant": a.variant, "n": a.n, "m": a.m, "s": a.s, "seed": a.seed,
         "dist": a.dist, **({"kappa": a.kappa} if a.dist == "geometric" else {}),
         "parallelism": f"row-sharded dp{world} (1-D ceil split), 1 allreduce per block step",
-        "collectives": ("NCCL" if world > 1 or getattr(a, "nccl", False)
+        "collectives": ("one-shot exchange over peer-mapped windows, fused with the step kernel"
+                        if getattr(a, "transport", "nccl") == "peer" else
+                        "NCCL" if world > 1 or getattr(a, "nccl", False)
                         else "none (one GPU: in-kernel reduction)"),
         "l2": f"inputs exceed L2: X is {a.n * a.m * 8 / 1e9:.2f} GB (126 MB L2), no flush needed",
     }
@@ -301,7 +308,15 @@ def run_ours(a):
         uid = obj[0]
     elif a.nccl:
         uid = bgs.nccl_unique_id()
-    ctx = bgs.Context(local, rank, world, uid)
+    if a.transport == "peer":
+        from paper_2507_21791_b200 import dist as bd
+        ctx = bgs.Context(local, rank, world, peer=True)
+        if world > 1:
+            bd.attach_peers(dist, ctx, 2)  # distinct GPUs: the flags are awaited in the kernel
+        else:
+            ctx.peer_attach([ctx.peer_handle()], 2)
+    else:
+        ctx = bgs.Context(local, rank, world, uid)
     v = int(bgs.parse_variant(a.variant))
     n, m, s = a.n, a.m, a.s
     row0, nl = bgs.shard_rows(n, world, rank)
