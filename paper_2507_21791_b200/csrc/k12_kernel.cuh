@@ -215,16 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     __syncwarp();
   } else {
     // ---------------- consumers: group g takes stages g, g+2, g+4, ... ----------------
-    // Coefficients, factors and the status word come from the preceding kernel.
-    griddep_wait();
-#if defined(BGS_STEP_STAMPS) && !defined(BGS_K12_NO_STAMPS)
-    const unsigned long long t_wait = k12_gtime();
-#endif
     const int g = warp / kGroupWarps, w = warp % kGroupWarps;
-    if (p.status && status_bad(p.status)) {
-      // an earlier step failed: drain the stages prefetched before the producer saw it
-      for (int it = g; it < pre; it += kGroups) mbar_wait(&full[it % S], (it / S) & 1);
-    } else {
     const int gtid = threadIdx.x - 32 * kGroupWarps * g;
     const int ii = lane >> 2, kk = lane & 3;
     const int gbar = 1 + g;
@@ -240,6 +231,85 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     const int ksteps = (kcols + 3) / 4;
     const int jlast = max(ksteps - 1, 0);
     const int kt_valid = kpart < ksteps ? (ksteps - 1 - kpart) / KS + 1 : 0;  // real k-steps
+    // Update A fragments: m-tile q, row index i is chunk row 4 f(i) + q with
+    // f(i) = (i >> 1) + 4 (i & 1), so lane (i, kk) reads rows 4f..4f+3 of tile column
+    // 4j + kk with two LDS.128 (line 8j + 2kk + (i & 1), 1024 j past k-step 0).  The two
+    // i of a quarter-warp sit in different 16-row halves -> chunk sets {2a ^ 2kk} and
+    // {2a ^ (2kk + 1)} are disjoint: conflict-free with no lane swap.
+    uint32_t uoff0, uoff1;
+    {
+      const int line = 2 * kk + (ii & 1);
+      const int rc = 2 * (ii >> 1);  // chunk of rows 4f, 4f + 1 inside the 16-row block
+      uoff0 = (uint32_t)(line * 128 + ((rc ^ (line & 7)) << 4));
+      uoff1 = (uint32_t)(line * 128 + (((rc + 1) ^ (line & 7)) << 4));
+    }
+    // local columns of the A block, the B block (= span-1 column 0) and the right operand
+    const bool a_own = p.kp >= 8 * own_u0 && p.kp < 8 * (own_u0 + own_n);
+    const int colA = a_own ? p.kp - 8 * own_u0 : 8 * own_n + p.kp - 8 * ext_u0;
+    const int colB = 8 * (own_n + ext_n);
+    const int rc = ii < p.N ? p.rcol1[ii] : -1;
+    const bool bval = rc >= 0;
+    const int bcol = colB + (bval ? rc : 0);
+    // output tiles of this rank: own units, then (rank 0) the span-1 left units
+    const int mt_loc = own_n + (rank == 0 ? p.s1_left : 0);
+    // Epilogue: warp w handles rows 8w + m (m = lane / 4) of every chunk (coalesced
+    // stores); in the update that row is m-tile q = m & 3, index i with
+    // f(i) = 2w + (m >> 2), of the chunk's quad.
+    const int erow = 8 * w + ii;
+    const int qsel = ii & 3, vsel = 2 * w + (ii >> 2), isel = 2 * (vsel & 3) + (vsel >> 2);
+    const int quad = lane & ~3;
+    // Per-lane epilogue plan, fixed for the whole kernel (the stage loop only adds the stage
+    // base and the row offset): lane (i, kk) reads z[row][kk] of both source blocks and owns
+    // output columns 2kk, 2kk + 1 (A for kk < 2, B for kk >= 2).  Recomputing these per stage
+    // cost ~250 cycles of a ~5000-cycle group-stage (33.8 -> 32.9 ms of fused time at config 2).
+    constexpr bool kEpPlan = MTW <= 6;  // (MTW >= 7: no registers to spare, measured)
+    const bool ep_isA = kk < 2;
+    const bool ep_za = p.upd_a && kk < s, ep_zb = p.upd_b && kk < s;
+    const uint32_t ep_offA = elem_off<2>(colA + kk, erow), ep_offB = elem_off<2>(colB + kk, erow);
+    const long ep_ld = ep_isA ? p.lddA : p.lddB;
+    uint32_t ep_so[2];  // shared-memory offsets of the two outputs inside a chunk
+    int ep_flags = 0;   // bit e: store output e to the stage; bit 2 + e: store it to HBM
+    {
+      const int c0 = ep_isA ? 2 * kk : 2 * kk - 4;
+      const bool on = ep_isA ? p.upd_a : p.upd_b;
+      // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
+      // shared: A only where its rows are output tiles (the rank owning the A units)
+      const bool gst = !pair || (ep_isA ? rank == 0 : rank == 1);
+      const bool sst = ep_isA ? (!pair || rank == 1) : true;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        ep_so[e] = elem_off<2>((ep_isA ? colA : colB) + c0 + e, erow);
+        if (on && c0 + e < s) ep_flags |= (sst ? 1 << e : 0) | (gst ? 4 << e : 0);
+      }
+    }
+    // HBM address of output 0 at shard row 0 of this lane's chunk row
+    double* const ep_g = (ep_isA ? p.dstA : p.dstB) + erow +
+                         (size_t)(ep_isA ? 2 * kk : 2 * kk - 4) * (size_t)ep_ld;
+    int acol[MTW];  // tile column of this lane's Gram fragment, per output tile
+    // (CT) compensated output tiles: global tile index >= p.comp_t0 -> every 4-row k-step
+    // goes straight into the double-double (BCGSI+1S: the U rows, DESIGN.md "Numerics")
+    bool ctile[MTW];
+#pragma unroll
+    for (int jj = 0; jj < MTW; ++jj) {
+      int t = w + kGroupWarps * jj;
+      const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
+      ctile[jj] = CT && t < mt_loc && tg >= p.comp_t0;
+      if (t >= mt_loc) t = w < mt_loc ? w : 0;
+      const int lu = t < own_n ? t : t + ext_n;
+      acol[jj] = 8 * lu + ii;
+    }
+
+    // Everything above depends on the launch parameters only and runs while the preceding
+    // kernel (the reduce + step) is still in flight; what follows reads its outputs.
+    // Coefficients, factors and the status word come from the preceding kernel.
+    griddep_wait();
+#if defined(BGS_STEP_STAMPS) && !defined(BGS_K12_NO_STAMPS)
+    const unsigned long long t_wait = k12_gtime();
+#endif
+    if (p.status && status_bad(p.status)) {
+      // an earlier step failed: drain the stages prefetched before the producer saw it
+      for (int it = g; it < pre; it += kGroups) mbar_wait(&full[it % S], (it / S) & 1);
+    } else {
     double bco[KW];
 #pragma unroll
     for (int t = 0; t < KW; ++t) {
@@ -301,75 +371,8 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       ep_m[l * 8 + j] = v;
     }
     bar_named(5, 32 * kConsWarps);
-    // Update A fragments: m-tile q, row index i is chunk row 4 f(i) + q with
-    // f(i) = (i >> 1) + 4 (i & 1), so lane (i, kk) reads rows 4f..4f+3 of tile column
-    // 4j + kk with two LDS.128 (line 8j + 2kk + (i & 1), 1024 j past k-step 0).  The two
-    // i of a quarter-warp sit in different 16-row halves -> chunk sets {2a ^ 2kk} and
-    // {2a ^ (2kk + 1)} are disjoint: conflict-free with no lane swap.
-    uint32_t uoff0, uoff1;
-    {
-      const int line = 2 * kk + (ii & 1);
-      const int rc = 2 * (ii >> 1);  // chunk of rows 4f, 4f + 1 inside the 16-row block
-      uoff0 = (uint32_t)(line * 128 + ((rc ^ (line & 7)) << 4));
-      uoff1 = (uint32_t)(line * 128 + (((rc + 1) ^ (line & 7)) << 4));
-    }
-    // local columns of the A block, the B block (= span-1 column 0) and the right operand
-    const bool a_own = p.kp >= 8 * own_u0 && p.kp < 8 * (own_u0 + own_n);
-    const int colA = a_own ? p.kp - 8 * own_u0 : 8 * own_n + p.kp - 8 * ext_u0;
-    const int colB = 8 * (own_n + ext_n);
-    const int rc = ii < p.N ? p.rcol1[ii] : -1;
-    const bool bval = rc >= 0;
-    const int bcol = colB + (bval ? rc : 0);
-    // output tiles of this rank: own units, then (rank 0) the span-1 left units
-    const int mt_loc = own_n + (rank == 0 ? p.s1_left : 0);
-    // Epilogue: warp w handles rows 8w + m (m = lane / 4) of every chunk (coalesced
-    // stores); in the update that row is m-tile q = m & 3, index i with
-    // f(i) = 2w + (m >> 2), of the chunk's quad.
-    const int erow = 8 * w + ii;
-    const int qsel = ii & 3, vsel = 2 * w + (ii >> 2), isel = 2 * (vsel & 3) + (vsel >> 2);
-    const int quad = lane & ~3;
     // epilogue matrix M as DMMA B fragments: lane (i, kk) holds M[kk][i] and M[4 + kk][i]
     const double mb0 = ep_m[kk * 8 + ii], mb1 = ep_m[(4 + kk) * 8 + ii];
-    // Per-lane epilogue plan, fixed for the whole kernel (the stage loop only adds the stage
-    // base and the row offset): lane (i, kk) reads z[row][kk] of both source blocks and owns
-    // output columns 2kk, 2kk + 1 (A for kk < 2, B for kk >= 2).  Recomputing these per stage
-    // cost ~250 cycles of a ~5000-cycle group-stage (33.8 -> 32.9 ms of fused time at config 2).
-    constexpr bool kEpPlan = MTW <= 6;  // (MTW >= 7: no registers to spare, measured)
-    const bool ep_isA = kk < 2;
-    const bool ep_za = p.upd_a && kk < s, ep_zb = p.upd_b && kk < s;
-    const uint32_t ep_offA = elem_off<2>(colA + kk, erow), ep_offB = elem_off<2>(colB + kk, erow);
-    const long ep_ld = ep_isA ? p.lddA : p.lddB;
-    uint32_t ep_so[2];  // shared-memory offsets of the two outputs inside a chunk
-    int ep_flags = 0;   // bit e: store output e to the stage; bit 2 + e: store it to HBM
-    {
-      const int c0 = ep_isA ? 2 * kk : 2 * kk - 4;
-      const bool on = ep_isA ? p.upd_a : p.upd_b;
-      // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
-      // shared: A only where its rows are output tiles (the rank owning the A units)
-      const bool gst = !pair || (ep_isA ? rank == 0 : rank == 1);
-      const bool sst = ep_isA ? (!pair || rank == 1) : true;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        ep_so[e] = elem_off<2>((ep_isA ? colA : colB) + c0 + e, erow);
-        if (on && c0 + e < s) ep_flags |= (sst ? 1 << e : 0) | (gst ? 4 << e : 0);
-      }
-    }
-    // HBM address of output 0 at shard row 0 of this lane's chunk row
-    double* const ep_g = (ep_isA ? p.dstA : p.dstB) + erow +
-                         (size_t)(ep_isA ? 2 * kk : 2 * kk - 4) * (size_t)ep_ld;
-    int acol[MTW];  // tile column of this lane's Gram fragment, per output tile
-    // (CT) compensated output tiles: global tile index >= p.comp_t0 -> every 4-row k-step
-    // goes straight into the double-double (BCGSI+1S: the U rows, DESIGN.md "Numerics")
-    bool ctile[MTW];
-#pragma unroll
-    for (int jj = 0; jj < MTW; ++jj) {
-      int t = w + kGroupWarps * jj;
-      const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
-      ctile[jj] = CT && t < mt_loc && tg >= p.comp_t0;
-      if (t >= mt_loc) t = w < mt_loc ? w : 0;
-      const int lu = t < own_n ? t : t + ext_n;
-      acol[jj] = 8 * lu + ii;
-    }
 
     // (hi, lo) double-double per output; the stage contractions accumulate in acc and are
     // folded in every kFold = 16 / R group-stages (<= 512 rows of plain fp64 per fold at

@@ -4,7 +4,7 @@
 # within 10x, identical sync accounting.  Optional BGS_POISON=1.  Prints failures.
 #   python tools/fuzz_parity.py [count] [seed]
 # FUZZ_NCCL=1: through bgs_factor_device on a one-rank NCCL context (the collective path;
-# procs = 1) instead of bgs_factor.
+# procs = 1) instead of bgs_factor.  FUZZ_PEER=1: the same on a one-rank peer-window context.
 import sys, time
 sys.path.insert(0, ".")
 import numpy as np
@@ -15,8 +15,15 @@ count = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 o = Oracle()
 import os
-nccl = os.environ.get("FUZZ_NCCL") == "1"
-if nccl:
+peer = os.environ.get("FUZZ_PEER") == "1"
+nccl = os.environ.get("FUZZ_NCCL") == "1" or peer
+if peer:
+    # a one-rank peer context with the in-kernel wait: the step fused with the exchange
+    # (reduce_xchg_step4_kernel) and the plain peer exchange on every other sync
+    import torch
+    ctx = bgs.Context(0, 0, 1, peer=True)
+    ctx.peer_attach([ctx.peer_handle()], 2)
+elif nccl:
     import torch
     ctx = bgs.Context(0, 0, 1, bgs.nccl_unique_id())
 else:
