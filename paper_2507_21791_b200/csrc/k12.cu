@@ -9,7 +9,7 @@ using namespace k12d;
 
 size_t k12_smem_bytes(int stages, int slot_units, int R, int C) {
   return 1024 + (size_t)stages * slot_units * R * kUnitChunkBytes + kRedBytes +
-         (C == 2 ? xchg_bytes(R) : 0) + (size_t)(2 * stages + 4) * sizeof(uint64_t);
+         (C >= 2 ? xchg_bytes(R, C) : 0) + (size_t)(2 * stages + 4) * sizeof(uint64_t);
 }
 
 // ------------------------------------------------------------------------------------
@@ -30,7 +30,8 @@ bool k12_plan(SplitParams& p) {
   p.s1_left = (p.lcols1 + 7) / 8;
   p.mt_out = p.U0 + p.s1_left;
   // C = 1 with the tallest stage that keeps >= 3 stages in shared memory, then the pair
-  const Cand cands[] = {{1, 4}, {1, 2}, {1, 1}, {2, 2}, {2, 1}};
+  // (clusters of 4: prefixes too wide for a pair, e.g. m = 800 late in the sweep)
+  const Cand cands[] = {{1, 4}, {1, 2}, {1, 1}, {2, 2}, {2, 1}, {4, 1}};
   // BGS_K12C_PLAN=CR (e.g. 21): only that candidate (tests / experiments; read per call)
   const char* fe = getenv("BGS_K12C_PLAN");
   const int forced = fe ? atoi(fe) : 0;
@@ -39,29 +40,43 @@ bool k12_plan(SplitParams& p) {
     SplitParams q = p;
     q.cluster = cd.C;
     q.R = cd.R;
-    int k0, k1 = 0, mt0, mt1 = 0;
+    int kmax = 0, mtmax = 0;  // most k-steps / output tiles of a rank
+    for (int r = 0; r < 4; ++r) q.own_u0[r] = q.own_n[r] = q.ext_u0[r] = q.ext_n[r] = 0;
     if (cd.C == 1) {
-      q.own_u0[0] = 0; q.own_n[0] = p.U0; q.ext_u0[0] = 0; q.ext_n[0] = 0;
-      q.own_u0[1] = q.own_n[1] = q.ext_u0[1] = q.ext_n[1] = 0;
+      q.own_n[0] = p.U0;
       q.slot_units = p.U0 + p.U1;
-      k0 = (p.kp + 3) / 4;
-      mt0 = p.U0 + q.s1_left;
+      kmax = (p.kp + 3) / 4;
+      mtmax = p.U0 + q.s1_left;
     } else {
-      const int uh = (p.U0 - na + 1) / 2;
-      q.own_u0[0] = 0;         q.own_n[0] = uh;
-      q.ext_u0[0] = p.U0 - na; q.ext_n[0] = na;
-      q.own_u0[1] = uh;        q.own_n[1] = p.U0 - uh;
-      q.ext_u0[1] = 0;         q.ext_n[1] = 0;
-      q.slot_units = std::max(uh + na, p.U0 - uh) + p.U1;
-      const int c0 = std::min(8 * uh, p.kp), c1 = std::max(0, p.kp - 8 * uh);
-      k0 = (c0 + 3) / 4;
-      k1 = (c1 + 3) / 4;
-      mt0 = uh + q.s1_left;
-      mt1 = p.U0 - uh;
+      // the prefix-only units split evenly over the ranks (the first ranks take the
+      // remainder); the last rank also owns the A-block units, the others load them as
+      // extra units: every rank forms B = (srcB - Qp CB - A S2) TB^-1 and needs srcA
+      const int nb = p.U0 - na;
+      if (cd.C == 2) {  // (the split of round 1: ceil / floor)
+        q.own_n[0] = (nb + 1) / 2;
+        q.own_n[1] = p.U0 - q.own_n[0];
+      } else {
+        for (int r = 0; r < cd.C; ++r) q.own_n[r] = nb / cd.C + (r < nb % cd.C ? 1 : 0);
+        q.own_n[cd.C - 1] += na;
+      }
+      int u = 0, units = 0;
+      for (int r = 0; r < cd.C; ++r) {
+        q.own_u0[r] = u;
+        u += q.own_n[r];
+        if (r < cd.C - 1) {
+          q.ext_u0[r] = p.U0 - na;
+          q.ext_n[r] = na;
+        }
+        units = std::max(units, q.own_n[r] + q.ext_n[r]);
+        const int c1 = std::min(8 * (q.own_u0[r] + q.own_n[r]), p.kp), c0 = std::min(8 * q.own_u0[r], p.kp);
+        kmax = std::max(kmax, (c1 - c0 + 3) / 4);
+        mtmax = std::max(mtmax, q.own_n[r] + (r == 0 ? q.s1_left : 0));
+      }
+      q.slot_units = units + p.U1;
     }
     const int KS = 4 / cd.R;
-    const int kw = (std::max(k0, k1) + KS - 1) / KS;
-    const int mtw = (std::max(mt0, mt1) + kGroupWarps - 1) / kGroupWarps;
+    const int kw = (kmax + KS - 1) / KS;
+    const int mtw = (mtmax + kGroupWarps - 1) / kGroupWarps;
     // one CTA at R = 1 carries up to kKwMaxR1 k-steps per warp while three stages fit
     // (BGS_K12C_KWMAX=16: the CTA pair takes those steps instead)
     const char* ke = getenv("BGS_K12C_KWMAX");
@@ -76,7 +91,7 @@ bool k12_plan(SplitParams& p) {
     // profiles/r01_stage_depth.log): the CTA-pair plans and the one-CTA R = 1 plans with
     // >= 6 output tiles per warp run 2-7% faster with 3 stages than with 4+; the taller
     // early stages (R = 2, 4) want 4.  BGS_K12C_MAXS overrides (experiments).
-    const int depth = (cd.C == 2 || (cd.R == 1 && mtw_for(kw_t, cd.R) >= 6)) ? 3 : 4;
+    const int depth = (cd.C >= 2 || (cd.R == 1 && mtw_for(kw_t, cd.R) >= 6)) ? 3 : 4;
     const char* xe = getenv("BGS_K12C_MAXS");
     const int max_s = std::max(min_s, xe ? std::min(kMaxStages, atoi(xe)) : depth);
     int S = 0;
@@ -106,6 +121,36 @@ bool k12_plan(SplitParams& p) {
 
 // k12_ct.cu
 cudaError_t k12_launch_ct(const SplitParams& p, int grid, cudaStream_t st);
+
+int k12_grid_cap(int C, int sms) {
+  if (C <= 2) return sms / C * C;
+  // clusters of 4: ask the driver how many fit at once with a full-size CTA (every K12c
+  // instance is one CTA per SM); a second wave of a few clusters would double the time
+  static int cached[2] = {0, 0};
+  int& c = cached[C == 4 ? 0 : 1];
+  if (!c) {
+    auto k = k12_kernel<13, mtw_for(13, 1), 1, false>;
+    const size_t smem = (size_t)kSmemOptin - kStaticSmem - 256;
+    int n = 0;
+    if (ensure_smem(k, smem) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(sms / C * C));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) n = 0;
+      (void)cudaGetLastError();
+    }
+    c = n > 0 ? n : sms / C * 7 / 8;
+  }
+  return std::min(sms / C, c) * C;
+}
 
 cudaError_t k12_launch(const SplitParams& p, int grid, cudaStream_t st, int* launches) {
   if (grid < p.cluster || grid % p.cluster) return cudaErrorInvalidValue;

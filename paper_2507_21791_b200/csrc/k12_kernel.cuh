@@ -60,7 +60,8 @@ constexpr int kProdRegs = 24, kConsRegs = 240;
 constexpr int kChunkRows = 32;
 constexpr int kUnitChunkBytes = 8 * kChunkRows * 8;  // one 8-column unit of one 32-row chunk
 constexpr int kRedBytes = kGroups * kGroupWarps * 4 * 32 * 16;  // [group][warp][m-tile][lane]
-__host__ __device__ constexpr int xchg_bytes(int R) { return kGroups * 2 * R * kGroupWarps * 32 * 16; }
+// exchange buffers of a cluster of C CTAs: [group][parity][source rank (C - 1)][chunk][warp][lane]
+__host__ __device__ constexpr int xchg_bytes(int R, int C = 2) { return (C - 1) * kGroups * 2 * R * kGroupWarps * 32 * 16; }
 constexpr int kStaticSmem = 2048;  // epilogue factor arrays (ptxas reports 2048 B static)
 constexpr int kSmemOptin = 232448;  // per-block opt-in maximum (227 KB)
 constexpr int kMaxStages = 8;
@@ -111,18 +112,19 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const bool pair = p.cluster == 2;
+  const int nrk = p.cluster;   // CTAs per cluster: 1, 2 or 4
+  const bool pair = nrk > 1;  // (a cluster splits the prefix columns over its CTAs)
   const int S = p.stages;
   const int chunk_bytes = p.slot_units * kUnitChunkBytes;
   const int slot_bytes = R * chunk_bytes;
   unsigned char* redbuf = smem + (size_t)S * slot_bytes;  // [group][warp][m-tile][lane]
   unsigned char* xbuf = redbuf + kRedBytes;               // [group][parity][chunk][warp][lane]
-  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + (pair ? xchg_bytes(R) : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + (pair ? xchg_bytes(R, nrk) : 0));
   uint64_t* empty = full + S;
   uint64_t* xfull = empty + S;  // [group][parity]
   __shared__ double ep_t[2][16], ep_s2[16], ep_ai[16], ep_bi[16], ep_w[16], ep_m[64];
 
-  const uint32_t rank = pair ? cluster_ctarank() : 0u, peer = rank ^ 1u;
+  const uint32_t rank = pair ? cluster_ctarank() : 0u;
 #ifdef BGS_CHECKED
   // every stage slot, the reduction and exchange buffers and the barriers inside the
   // dynamic allocation (the host sized it with k12_smem_bytes)
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     uint32_t dyn;
     asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     const size_t need = (size_t)(smem - smem_raw) + (size_t)S * slot_bytes + kRedBytes +
-                        (pair ? xchg_bytes(R) : 0) + (2 * S + 4) * sizeof(uint64_t);
+                        (pair ? xchg_bytes(R, nrk) : 0) + (2 * S + 4) * sizeof(uint64_t);
     BGS_DCHECK(need <= dyn, "k12: shared-memory layout exceeds the allocation");
     BGS_DCHECK(p.own_n[rank] + p.ext_n[rank] + p.U1 <= p.slot_units, "k12: units exceed the slot");
     BGS_DCHECK(S >= 1 && S <= kMaxStages, "k12: ring depth");
@@ -141,8 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
   const int nloc = own_n + ext_n + p.U1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long T = p.total_stages;
-  const int cl = pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int ncl = pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int cl = (int)blockIdx.x / nrk;
+  const int ncl = (int)gridDim.x / nrk;
   const long st0 = (long)cl * T / ncl;
   const int nst = (int)((long)(cl + 1) * T / ncl - st0);
   const int s = p.s;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
       // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
       // shared: A only where its rows are output tiles (the rank owning the A units)
       const bool gst = !pair || (ep_isA ? rank == 0 : rank == 1);
-      const bool sst = ep_isA ? (!pair || rank == 1) : true;
+      const bool sst = ep_isA ? (!pair || (int)rank == nrk - 1) : true;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         ep_so[e] = elem_off<2>((ep_isA ? colA : colB) + c0 + e, erow);
@@ -503,24 +505,47 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         }
       }
       if (pair) {
-        // ---- exchange with the same warp of the peer rank (DSMEM) ----
+        // ---- exchange with the same warp of every peer rank (DSMEM); rank q's partial lands
+        // in source slot (q < r ? q : q - 1) of rank r ----
         const int xb = g * 2 + (j & 1);
-        const uint32_t rbar = mapa_shared(xfull_local + (uint32_t)(xb * 8), peer);
 #pragma unroll
-        for (int ch = 0; ch < R; ++ch) {
-          const uint32_t mine =
-              xb_local + (uint32_t)((((xb * R + ch) * kGroupWarps + w) * 32 + lane) * 16);
-          st_async_v2f64(mapa_shared(mine, peer), D0[ch], D1[ch], rbar);
+        for (int q = 0; q < 4; ++q) {
+          if (q >= nrk || q == (int)rank) continue;
+          const int src = (int)rank < q ? (int)rank : (int)rank - 1;
+          const uint32_t rbar = mapa_shared(xfull_local + (uint32_t)(xb * 8), (uint32_t)q);
+#pragma unroll
+          for (int ch = 0; ch < R; ++ch) {
+            const uint32_t dst = xb_local + (uint32_t)((((((xb * (nrk - 1) + src) * R + ch) * kGroupWarps + w) * 32 + lane) * 16));
+            st_async_v2f64(mapa_shared(dst, (uint32_t)q), D0[ch], D1[ch], rbar);
+          }
         }
-        if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], R * kGroupWarps * 32 * 16);
+        if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], (nrk - 1) * R * kGroupWarps * 32 * 16);
         mbar_wait(&xfull[xb], (j >> 1) & 1);  // data and completion are both CTA-local
+        // every rank adds the partials in rank order 0, 1, ...: identical bits on all of them
+        // (two ranks: own + other, as IEEE addition commutes)
 #pragma unroll
         for (int ch = 0; ch < R; ++ch) {
-          const uint32_t mine =
-              xb_local + (uint32_t)((((xb * R + ch) * kGroupWarps + w) * 32 + lane) * 16);
-          const double2 o = lds128(mine);
-          D0[ch] += o.x;  // IEEE addition commutes: both ranks hold (rank 0) + (rank 1)
-          D1[ch] += o.y;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q >= nrk) continue;
+            double2 v;
+            if (q == (int)rank) {
+              v = make_double2(D0[ch], D1[ch]);
+            } else {
+              const int src = q < (int)rank ? q : q - 1;
+              v = lds128(xb_local + (uint32_t)((((((xb * (nrk - 1) + src) * R + ch) * kGroupWarps + w) * 32 + lane) * 16)));
+            }
+            if (q == 0) {
+              a0 = v.x;
+              a1 = v.y;
+            } else {
+              a0 += v.x;
+              a1 += v.y;
+            }
+          }
+          D0[ch] = a0;
+          D1[ch] = a1;
         }
       }
       if (prof) { const unsigned long long t = clock64(); ph[2] += t - t1; t1 = t; if (tl && j < kTl) tl[j * 6 + 3] = t; }
@@ -576,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
           // global stores: rank 0 writes A, rank 1 writes B (C = 1: rank 0 writes both);
           // shared: A only where its rows are output tiles (the rank owning the A units)
           const bool gstore = live && (!pair || (isA ? rank == 0 : rank == 1));
-          const bool sstore = isA ? (!pair || rank == 1) : true;
+          const bool sstore = isA ? (!pair || (int)rank == nrk - 1) : true;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int c = c0 + e;
@@ -703,9 +728,9 @@ static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   int na = 0;
-  if (p.cluster == 2) {
+  if (p.cluster > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.x = (unsigned)p.cluster;
     at[na].val.clusterDim.y = 1;
     at[na].val.clusterDim.z = 1;
     ++na;

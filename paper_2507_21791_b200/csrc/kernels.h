@@ -77,8 +77,8 @@ struct alignas(64) SplitParams {
   int ncols0;           // columns of span 0 (all are output rows)
   int lcols1;           // output-row columns of span 1 (rank 0 emits them)
   int s1_left;          // ceil(lcols1 / 8)
-  int own_u0[2], own_n[2];  // per cluster rank: owned span-0 units
-  int ext_u0[2], ext_n[2];  // per cluster rank: extra span-0 units (the A block)
+  int own_u0[4], own_n[4];  // per cluster rank: owned span-0 units
+  int ext_u0[4], ext_n[4];  // per cluster rank: extra span-0 units (the A block)
   int slot_units;       // max local units over the two ranks
   int mt_out;           // global 8-column output tiles (U0 + s1_left)
   int N;                // right-operand columns (<= 8), all in span 1
@@ -86,7 +86,7 @@ struct alignas(64) SplitParams {
   long n_rows;
   long total_stages;    // 32-row stages of the shard
   int stages;           // ring depth
-  int cluster;          // CTAs per cluster: 1 (whole tile per CTA) or 2 (split prefix)
+  int cluster;          // CTAs per cluster: 1 (whole tile per CTA), 2 or 4 (split prefix)
   int R;                // 32-row chunks per stage (1, 2, 4)
   int kw, mtw;          // k-steps / output tiles per warp (planned; selects the instance)
   int upd_a, upd_b, kp, s;
@@ -106,6 +106,9 @@ struct alignas(64) SplitParams {
 bool k12_plan(SplitParams& p);
 size_t k12_smem_bytes(int stages, int slot_units, int R, int C);
 cudaError_t k12_launch(const SplitParams& p, int grid, cudaStream_t st, int* launches);
+// CTAs a launch of cluster width C may use: C x the clusters that can be co-resident
+// (clusters of 4 do not tile all 148 SMs), at most `sms`
+int k12_grid_cap(int C, int sms);
 
 // ---------------- K2: block update (update.cu) ----------------
 struct UpdateParams {

@@ -825,7 +825,7 @@ class Runner {
     const size_t per_slot = gram_partial_doubles_per_cta(p.mt_out, p.N);
     int slot_base = 0;
     for (auto& x : sh) {
-      const int grid = p.cluster == 2 ? grid_for(x) & ~1 : grid_for(x);
+      const int grid = p.cluster >= 2 ? std::min(grid_for(x) / p.cluster * p.cluster, k12_grid_cap(p.cluster, c->sms)) : grid_for(x);
       if (x.rows > 0) {
         for (int wi = 0; wi < 5; ++wi)
           p.map0[wi] = sp.sp[0].src == SX ? x.mapX[0][wi] : x.mapQ[0][wi];

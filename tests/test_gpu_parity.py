@@ -393,7 +393,7 @@ def test_streamed_host_io_is_bitwise_identical(gpu_ctx, monkeypatch, v, procs):
     assert np.array_equal(r, staged.r)
 
 
-@pytest.mark.parametrize("plan", ["14", "12", "11", "22", "21"])
+@pytest.mark.parametrize("plan", ["14", "12", "11", "22", "21", "41"])
 @pytest.mark.parametrize("v", [3, 2, 5], ids=lambda v: NAMES[v])
 def test_fused_plans_match_oracle(oracle, gpu_ctx, monkeypatch, v, plan):
     """Every K12c plan (cluster width C, 32-row chunks per stage R; BGS_K12C_PLAN=CR)
@@ -411,6 +411,25 @@ def test_fused_plans_match_oracle(oracle, gpu_ctx, monkeypatch, v, plan):
     assert_r_close(out.r, ref.r)
     assert oracle.loo(out.q) <= 10 * max(ref.loo, U)
     assert oracle.residual(x, out.q, out.r) <= 10 * max(ref.resid, U)
+
+
+def test_cluster_of_four_agrees_with_the_pair(oracle, gpu_ctx, monkeypatch):
+    """Clusters of 4 (prefixes too wide for a CTA pair: m = 800 late in a sweep) exchange the
+    partial update among four CTAs and add it in rank order.  On a shape both can take, the
+    forced cluster-of-4 plan agrees with the forced pair plan to rounding (the k-ranges are
+    cut differently), is deterministic run to run, and matches the oracle."""
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 30011, 256, 4
+    x = oracle.gen_matrix(n, m, s, 1e2, 99, True)
+    monkeypatch.setenv("BGS_K12C_PLAN", "21")
+    pair = bgs.run_factor(3, x, s, 1, metrics=False)
+    monkeypatch.setenv("BGS_K12C_PLAN", "41")
+    quad = bgs.run_factor(3, x, s, 1, metrics=False)
+    quad2 = bgs.run_factor(3, x, s, 1, metrics=False)
+    assert pair.ok and quad.ok
+    assert np.array_equal(quad.q, quad2.q) and np.array_equal(quad.r, quad2.r)
+    assert np.abs(quad.r - pair.r).max() <= 1e-13 * np.abs(pair.r).max()
+    assert oracle.loo(quad.q) <= 10 * max(oracle.loo(pair.q), U)
 
 
 def test_fused_plans_agree_bitwise_across_procs_splits(gpu_ctx, monkeypatch):
