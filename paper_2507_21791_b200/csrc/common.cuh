@@ -42,6 +42,7 @@ enum StatusCode : int {
   ST_NOT_SPD = 2,
   ST_SINGULAR = 3,
   ST_NON_FINITE = 5,
+  ST_COLLECTIVE = 6,  // the peer exchange's in-kernel wait gave up (a rank never published its flag)
 };
 // Sites of rethrow_not_spd (bcgs.cpp:284, 325, 356, 194, 209).
 enum Site : int {
@@ -191,6 +192,23 @@ BGS_DEV unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+// Bounded acquire spin on a flag of the peer exchange: until *f reached `epoch`, or ~8 s of
+// %globaltimer went by (a rank that died or never joined must not hang this GPU): false on
+// timeout.
+BGS_DEV bool spin_flag_geq(const unsigned* f, unsigned epoch) {
+  unsigned long long t0 = 0;
+  for (unsigned it = 0; (int)(ld_acquire_sys(f) - epoch) < 0; ++it) {
+    __nanosleep(20);
+    if ((it & 1023u) == 1023u) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 8000000000ull) return false;
+    }
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------------------------

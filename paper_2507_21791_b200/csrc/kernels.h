@@ -246,8 +246,11 @@ cudaError_t peer_push_launch(const PeerView& v, const double* a, unsigned long n
                              int* launches);
 // recv[r * ng + i] = rank r's gather part; sum[i] = the ns partials added in rank order.
 // spin: wait in the kernel for the P flags (distinct GPUs only).
+// status (optional): the in-kernel wait gives up after ~8 s and records ST_COLLECTIVE there.
+struct DevStatus;
 cudaError_t peer_sum_launch(const PeerView& v, unsigned long ng, double* recv, unsigned long ns,
-                            double* sum, unsigned epoch, bool spin, cudaStream_t st, int* launches);
+                            double* sum, unsigned epoch, bool spin, cudaStream_t st, int* launches,
+                            DevStatus* status = nullptr);
 
 // The one-sync step fused with the exchange (small.cu): A = reduce + push + flags, B =
 // [spin] + rank-ordered sum + step, AB = both in one launch (in-kernel spin).

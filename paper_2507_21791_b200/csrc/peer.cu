@@ -58,12 +58,14 @@ __global__ void __launch_bounds__(512) peer_push_kernel(const PeerView v, const 
 __global__ void __launch_bounds__(512) peer_sum_kernel(const PeerView v, unsigned long ng,
                                                        double* __restrict__ recv, unsigned long ns,
                                                        double* __restrict__ sum, unsigned epoch,
-                                                       int spin) {
+                                                       int spin, DevStatus* status) {
   unsigned char* win = v.win[v.rank];
   if (spin) {
     if ((int)threadIdx.x < v.P) {
       const unsigned* f = reinterpret_cast<const unsigned*>(win) + threadIdx.x;
-      while ((int)(ld_acquire_sys(f) - epoch) < 0) __nanosleep(20);
+      if (!spin_flag_geq(f, epoch) && status) {  // (first writer wins, like every status)
+        if (atomicCAS(&status->code, 0, (int)ST_COLLECTIVE) == 0) status->pivot = (int)threadIdx.x + 1;
+      }
     }
     __syncthreads();
   }
@@ -96,10 +98,11 @@ cudaError_t peer_push_launch(const PeerView& v, const double* a, unsigned long n
 }
 
 cudaError_t peer_sum_launch(const PeerView& v, unsigned long ng, double* recv, unsigned long ns,
-                            double* sum, unsigned epoch, bool spin, cudaStream_t st, int* launches) {
+                            double* sum, unsigned epoch, bool spin, cudaStream_t st, int* launches,
+                            DevStatus* status) {
   const unsigned long w = std::max(ns, ng * (unsigned long)v.P);
   const int G = (int)std::min<unsigned long>(32, std::max<unsigned long>(1, (w + 2047) / 2048));
-  peer_sum_kernel<<<G, 512, 0, st>>>(v, ng, recv, ns, sum, epoch, spin ? 1 : 0);
+  peer_sum_kernel<<<G, 512, 0, st>>>(v, ng, recv, ns, sum, epoch, spin ? 1 : 0, status);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

@@ -735,7 +735,8 @@ class Runner {
       }
       ++waits;
     }
-    CUDA_OK(peer_sum_launch(pc.view, ng, recv, ns, sum, ep, pc.wait_mode == 2, c->stream, &c->launches));
+    CUDA_OK(peer_sum_launch(pc.view, ng, recv, ns, sum, ep, pc.wait_mode == 2, c->stream, &c->launches,
+                            status));
   }
 
   // RecurrenceProbe::on_eval (bcgs.cpp:339-343): S2 of step k and this rank's rows of Q_k
@@ -1785,6 +1786,10 @@ class Runner {
       if (getenv("BGS_DEBUG_STATUS")) f.msg += " (block column " + std::to_string(h.block) + ")";
     } else if (h.code == ST_SINGULAR) {
       f.msg = "triangular factor has a zero at diagonal entry " + std::to_string(h.pivot);
+    } else if (h.code == ST_COLLECTIVE) {
+      f.msg = "peer exchange: rank " + std::to_string(h.pivot - 1) +
+              " never published its flag (gave up after ~8 s; rank " + std::to_string(c->rank) + " of " +
+              std::to_string(c->nranks) + ")";
     } else {
       f.msg = "device status " + std::to_string(h.code);
     }

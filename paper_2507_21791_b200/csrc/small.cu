@@ -811,12 +811,13 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 // A block step is then fused kernel -> A -> B (or AB) -> fused kernel instead of fused ->
 // gram_reduce -> push -> sum -> step -> fused.
 BGS_DEV void peer_sum_body(const PeerView& v, unsigned epoch, int spin, unsigned long words,
-                           double* __restrict__ G) {
+                           double* __restrict__ G, DevStatus* status) {
   unsigned char* win = v.win[v.rank];
   if (spin) {
     if ((int)threadIdx.x < v.P) {
       const unsigned* f = reinterpret_cast<const unsigned*>(win) + threadIdx.x;
-      while ((int)(ld_acquire_sys(f) - epoch) < 0) __nanosleep(20);
+      if (!spin_flag_geq(f, epoch) && status)  // (pivot: the rank that never arrived, 1-based)
+        set_status(status, ST_COLLECTIVE, (int)threadIdx.x + 1, 0, SITE_NONE, 0);
     }
     __syncthreads();
   }
@@ -861,7 +862,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     sum_step4_kernel(const PeerView v, unsigned epoch, int spin, unsigned long words, double* G,
                      SmallParams p, unsigned* ticket) {
   griddep_launch_dependents();
-  peer_sum_body(v, epoch, spin, words, G);
+  peer_sum_body(v, epoch, spin, words, G, const_cast<DevStatus*>(p.status));
   if (!last_cta(ticket, false)) return;
   onesync_step4_body(p);
 }
@@ -876,7 +877,7 @@ __global__ void __launch_bounds__(kStepThreads, 1)
   // (every CTA of this grid is resident -- one wave -- so the spin cannot starve the CTA
   // that publishes this rank's flag; the peers' flags arrive over NVLink)
   __syncthreads();
-  peer_sum_body(v, epoch, 1, words, G);
+  peer_sum_body(v, epoch, 1, words, G, const_cast<DevStatus*>(p.status));
   if (!last_cta(ticket + 1, false)) return;
   onesync_step4_body(p);
 }
