@@ -290,12 +290,20 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     int acol[MTW];  // tile column of this lane's Gram fragment, per output tile
     // (CT) compensated output tiles: global tile index >= p.comp_t0 -> every 4-row k-step
     // goes straight into the double-double (BCGSI+1S: the U rows)
-    bool ctile[MTW];
+    // The compensated tile of a fused step is always the span-1 left unit on rank 0
+    // (U_{k+1} and X_{k+2} as output rows; the runtime plans K12c only for that layout).  It
+    // is shared by the four warps of a group: warp w takes the 4-row k-steps q4 = w of
+    // every row pass into its own double-double (coop_*), outside the branch-free tile
+    // loop -- a per-tile flag tested at every DMMA split that loop into basic blocks and
+    // made every step ~1.5x slower -- and the partials of the 8 warps are added in a fixed
+    // order at the end.
+    const bool coop = CT && p.comp_t0 == p.U0 && p.mt_out - p.comp_t0 == 1 && rank == 0 && p.s1_left == 1;
+    const int coop_col = 8 * (own_n + ext_n) + ii;  // the tile's column of this lane (span-1 unit 0)
+    // (one double-double per row pass u: two independent two_sum chains per warp)
+    double coop_hi[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, coop_lo[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int jj = 0; jj < MTW; ++jj) {
       int t = w + kGroupWarps * jj;
-      const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
-      ctile[jj] = CT && t < mt_loc && tg >= p.comp_t0;
       if (t >= mt_loc) t = w < mt_loc ? w : 0;
       const int lu = t < own_n ? t : t + ext_n;
       acol[jj] = 8 * lu + ii;
@@ -390,17 +398,6 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     for (int j = 0; j < MTW; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) hi[j][e] = lo[j][e] = acc[j][e] = 0.0;
-    // one 4-row DMMA k-step of a compensated tile, folded into (hi, lo) at once
-    auto dmma_dd = [&](int jj, double a, double b) {
-      double c0 = 0.0, c1 = 0.0, sm, err;
-      dmma(c0, c1, a, b);
-      two_sum(hi[jj][0], c0, sm, err);
-      hi[jj][0] = sm;
-      lo[jj][0] += err;
-      two_sum(hi[jj][1], c1, sm, err);
-      hi[jj][1] = sm;
-      lo[jj][1] += err;
-    };
     auto fold = [&]() {
 #pragma unroll
       for (int jj = 0; jj < MTW; ++jj)
@@ -649,13 +646,28 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
             const bool v1 = !kSkipPad || jp + 1 < MTW - 2 || w + kGroupWarps * (jp + 1) < mt_loc;
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
-              if (CT && ctile[jp]) dmma_dd(jp, a0[q4], b[q4]);
-              else if (v0) dmma(acc[jp][0], acc[jp][1], a0[q4], b[q4]);
+              if (v0) dmma(acc[jp][0], acc[jp][1], a0[q4], b[q4]);
               if (jp + 1 < MTW) {
-                if (CT && ctile[jp + 1]) dmma_dd(jp + 1, a1[q4], b[q4]);
-                else if (v1) dmma(acc[jp + 1][0], acc[jp + 1][1], a1[q4], b[q4]);
+                if (v1) dmma(acc[jp + 1][0], acc[jp + 1][1], a1[q4], b[q4]);
               }
             }
+          }
+          if (CT && coop) {
+            // this warp's k-step (q4 = w) of the shared compensated tile: one 16-byte
+            // fragment chunk (rows 4u'.. of the pass) and the matching right fragment
+            const int line = 2 * coop_col + gh;
+            const double2 x = lds128(cb + (uint32_t)(line * 128) +
+                                     (uint32_t)(((rcu + (w >> 1)) ^ (line & 7)) << 4));
+            const double av = (w & 1) ? x.y : x.x;
+            const double bv = w == 0 ? b[0] : w == 1 ? b[1] : w == 2 ? b[2] : b[3];
+            double c0 = 0.0, c1 = 0.0, sm, err;
+            dmma(c0, c1, av, bv);
+            two_sum(coop_hi[u][0], c0, sm, err);
+            coop_hi[u][0] = sm;
+            coop_lo[u][0] += err;
+            two_sum(coop_hi[u][1], c1, sm, err);
+            coop_hi[u][1] = sm;
+            coop_lo[u][1] += err;
           }
         }
       }
@@ -684,14 +696,40 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         for (int e = 0; e < 2; ++e)
           sts128(park + (uint32_t)((((w * MTW + jj) * 2 + e) * 32 + lane) * 16), hi[jj][e], lo[jj][e]);
     }
+    // the shared compensated tile: every warp's partial, [group][warp][element][lane]
+    const uint32_t cpark = park + (uint32_t)(kGroupWarps * MTW * 2 * 32 * 16);
+    if (CT && coop) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {  // the two row passes first (u = 0, then u = 1)
+        double sm, err;
+        two_sum(coop_hi[0][e], coop_hi[1][e], sm, err);
+        sts128(cpark + (uint32_t)((((g * kGroupWarps + w) * 2 + e) * 32 + lane) * 16), sm,
+               err + (coop_lo[0][e] + coop_lo[1][e]));
+      }
+    }
     bar_named(3, 32 * kConsWarps);
+    if (CT && coop && g == 0 && w == 0) {
+      double2* part = reinterpret_cast<double2*>(p.partial) + (size_t)cl * p.mt_out * 64;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double h = 0.0, l = 0.0;
+        for (int i = 0; i < kGroups * kGroupWarps; ++i) {  // fixed order: group 0 warps 0..3, group 1 ...
+          const double2 o = lds128(cpark + (uint32_t)(((i * 2 + e) * 32 + lane) * 16));
+          double sm, err;
+          two_sum(h, o.x, sm, err);
+          h = sm;
+          l += err + o.y;
+        }
+        part[((size_t)p.comp_t0 * 8 + ii) * 8 + 2 * kk + e] = make_double2(h, l);
+      }
+    }
     if (g == 0) {
       double2* part = reinterpret_cast<double2*>(p.partial) + (size_t)cl * p.mt_out * 64;
 #pragma unroll
       for (int jj = 0; jj < MTW; ++jj) {
         const int t = w + kGroupWarps * jj;
-        if (t < mt_loc) {
-          const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
+        const int tg = t < own_n ? own_u0 + t : p.U0 + (t - own_n);
+        if (t < mt_loc && !(CT && coop && tg == p.comp_t0)) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const double2 o = lds128(park + (uint32_t)((((w * MTW + jj) * 2 + e) * 32 + lane) * 16));

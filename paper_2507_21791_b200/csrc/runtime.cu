@@ -796,6 +796,8 @@ class Runner {
     p.s = (int)s;
     if (!k12_plan(p)) return false;
     p.comp_t0 = comp_tile(sp, sp.sp[0].ncols, p.U0, p.mt_out);
+    // K12c compensates exactly the span-1 left unit (U_{k+1}, X_{k+2} as output rows)
+    if (p.comp_t0 < p.mt_out && !(p.comp_t0 == p.U0 && p.s1_left == 1)) return false;
     for (auto& x : sh)
       if (x.rows > 0 && grid_for(x) < p.cluster) return false;
     return true;

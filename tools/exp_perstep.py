@@ -11,7 +11,7 @@ ctx = bgs.Context(0)
 X = torch.empty((m, ld), dtype=torch.float64, device="cuda")
 Q = torch.empty((m, ld), dtype=torch.float64, device="cuda")
 bgs.gen_gaussian_device(ctx, 12345, 0, n, m, X.data_ptr(), ld)
-v = int(bgs.parse_variant("BCGSI+P-1S"))
+v = int(bgs.parse_variant(os.environ.get("VARIANT", "BCGSI+P-1S")))
 for rep in range(2):
     ctx.profile(True)
     bgs.factor_device(ctx, v, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
