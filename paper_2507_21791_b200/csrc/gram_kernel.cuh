@@ -191,11 +191,14 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant
   for (int j = 0; j < MTW; ++j) acol[j] = 8 * (j < cnt ? cw + WG * j : 0) + ii;
   // (CT) the compensated tile of this warp (tiles >= p.comp_t0; at most one per warp: the
   // runtime keeps the range <= WG tiles): each 4-row k-step goes straight into (chi, clo)
-  int cj = -1;
+  int cj = -1, acolc = ii;
   if (CT) {
 #pragma unroll
     for (int j = 0; j < MTW; ++j)
-      if (j < cnt && cw + WG * j >= p.comp_t0 && cj < 0) cj = j;
+      if (j < cnt && cw + WG * j >= p.comp_t0 && cj < 0) {
+        cj = j;
+        acolc = 8 * (cw + WG * j) + ii;
+      }
   }
   double chi[CT ? NT : 1][2], clo[CT ? NT : 1][2];
 #pragma unroll
@@ -413,20 +416,29 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(const __grid_constant
 #pragma unroll
           for (int j = 0; j < MTW; ++j)
 #pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[j][nt][0], acc[j][nt][1], a[j][q4], b[nt][q4]);
+        // (CT) this warp's compensated tile again, each 4-row k-step straight into
+        // (chi, clo): outside the loop above, which stays branch-free (a flag tested at
+        // every DMMA split it into basic blocks: BCGSI+1S at s = 8 / 16 57 / 60 ms against
+        // 40 / 39 for P-1S); the plain sums of that tile are dropped at the end
+        if (CT && cj >= 0) {
+          double ac[4];
+          frag4<H>(base, acolc, h, kk, odd, ac);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-              if (CT && j == cj) {
-                double c0 = 0.0, c1 = 0.0, sm, err;
-                dmma(c0, c1, a[j][q4], b[nt][q4]);
-                two_sum(chi[CT ? nt : 0][0], c0, sm, err);
-                chi[CT ? nt : 0][0] = sm;
-                clo[CT ? nt : 0][0] += err;
-                two_sum(chi[CT ? nt : 0][1], c1, sm, err);
-                chi[CT ? nt : 0][1] = sm;
-                clo[CT ? nt : 0][1] += err;
-              } else {
-                dmma(acc[j][nt][0], acc[j][nt][1], a[j][q4], b[nt][q4]);
-              }
+              double c0 = 0.0, c1 = 0.0, sm, err;
+              dmma(c0, c1, ac[q4], b[nt][q4]);
+              two_sum(chi[CT ? nt : 0][0], c0, sm, err);
+              chi[CT ? nt : 0][0] = sm;
+              clo[CT ? nt : 0][0] += err;
+              two_sum(chi[CT ? nt : 0][1], c1, sm, err);
+              chi[CT ? nt : 0][1] = sm;
+              clo[CT ? nt : 0][1] += err;
             }
+        }
       }
     }
     if (prof) { const unsigned long long t = clock64(); ph[4] += t - t1; t1 = t; }
