@@ -129,7 +129,7 @@ int update_max_kp(int s);
 
 // ---------------- K2m: the s = 8 / 16 update fed by TMA (update_tma.cu) ----------------
 struct alignas(64) UpdTmaParams {
-  CUtensorMap map[5];  // the Q buffer, 3-D boxes {16, 4, w}, w = 128/64/32/16/8
+  CUtensorMap map[5];  // the Q buffer, 3-D boxes {16, 2, w}, w = 128/64/32/16/8
   int col0;            // first prefix column in the map
   long n_rows;
   long total_blocks;   // 32-row blocks (set by the launcher)

@@ -1158,7 +1158,7 @@ class Runner {
           const bool last = c1 == u.kp;
           UpdTmaParams q;
           memset(&q, 0, sizeof q);
-          for (int wi = 0; wi < 5; ++wi) q.map[wi] = x.mapQ[1][wi];  // boxes {16, 4, w}
+          for (int wi = 0; wi < 5; ++wi) q.map[wi] = x.mapQ[0][wi];  // boxes {16, 2, w}
           q.col0 = c0;
           q.n_rows = x.rows;
           q.kp = c1 - c0;

@@ -7,8 +7,8 @@
 // latency-bound at 0.3-0.45 of the roofline (ncu: 20% occupancy, 32% / 20% DRAM at
 // s = 8 / 16, profiles/r02_ncu_k2t.md).  Here:
 //  * a persistent CTA per SM walks 64-row blocks of its shard; the prefix Q[:, 0:kp] of a
-//    block streams through a ring of k-chunk stages (64 rows x 32 columns, 3-D TMA boxes
-//    {16, 4, w}: 512-byte runs per column, SWIZZLE_128B; as many 16 KB stages as shared
+//    block streams through a ring of k-chunk stages (64 rows x 32 columns as two 32-row
+//    quads, 3-D TMA boxes {16, 2, w}: 256-byte runs per column, SWIZZLE_128B; as many 16 KB stages as shared
 //    memory holds next to the coefficients), one producer thread;
 //  * the coefficients [CA | CB] (kp x 2S) sit in shared memory in DMMA-fragment order for
 //    the whole kernel;
@@ -37,6 +37,7 @@ constexpr int kUmThreads = 32 * (kUmWarps + kUmEpi + 1);
 constexpr int kUmRows = 64;                          // rows per block (two 32-row quads)
 constexpr int kUmKC = 32;                            // prefix columns per stage
 constexpr int kUmStageBytes = kUmKC * kUmRows * 8;   // 16 KB
+constexpr int kUmQuadBytes = kUmKC * 32 * 8;         // a stage is two 32-row quads, quad-major
 constexpr int kUmStagesMax = 8;  // ring depth: as many 16 KB stages as fit (>= 3)
 constexpr int kUmBufs = kUmEpi;                      // D scratch buffers (one per epilogue warp)
 constexpr int kUmSmemMax = 232448 - 1024;
@@ -190,12 +191,14 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
           mbar_arrive_expect_tx(&full[slot], (uint32_t)(w * kUmRows * 8));
           unsigned char* dst = smem + (size_t)slot * kUmStageBytes;
           int done = 0;
-          while (done < w) {  // greedy boxes {16, 4, 32 / 16 / 8}: 512-byte runs per column
+          while (done < w) {  // greedy boxes {16, 2, 32 / 16 / 8}, one per 32-row quad
             const int left = w - done;
             const int wi = left >= 32 ? 2 : left >= 16 ? 3 : 4;
             BGS_DCHECK(done + (128 >> wi) <= kUmKC, "k2m: TMA box past the stage");
-            tma_load_3d(dst + (size_t)done * 512, &p.map[wi], &full[slot], 0, (int)(4 * b),
-                        p.col0 + c0 + done);
+#pragma unroll
+            for (int qd = 0; qd < 2; ++qd)
+              tma_load_3d(dst + (size_t)qd * kUmQuadBytes + (size_t)done * 256, &p.map[wi],
+                          &full[slot], 0, (int)(4 * b + 2 * qd), p.col0 + c0 + done);
             done += 128 >> wi;
           }
         }
@@ -293,10 +296,14 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   const int ii = lane >> 2, kk = lane & 3;
   // m-tile q of quad qd, row index i is block row 32 qd + 4 f(i) + q with
   // f(i) = (i >> 1) + 4 (i & 1): two LDS.128 give lane (i, kk) its 4 rows of k-step column
-  // 4j + kk (k12.cu's conflict-free scheme, on the {16, 4, w} layout: line 4c + h)
+  // 4j + kk (k12.cu's conflict-free scheme on K12c's {16, 2, w} quad layout: line 2c + h, so
+  // the four kk of a quarter-warp hit four distinct 16-byte chunk positions.  The first K2m
+  // kept the 64 rows of a column together ({16, 4, w}: line 4c + h), where kk = 0, 2 and
+  // 1, 3 collide: every fragment load took two wavefronts; ncu showed the shared pipe at
+  // 79% and the DMMA pipe at 48% at s = 16)
   uint32_t uoff0, uoff1;
   {
-    const int line = 4 * kk + 2 * qd + (ii & 1);
+    const int line = 2 * kk + (ii & 1);
     const int rc = 2 * (ii >> 1);
     uoff0 = (uint32_t)(line * 128 + ((rc ^ (line & 7)) << 4));
     uoff1 = (uint32_t)(line * 128 + (((rc + 1) ^ (line & 7)) << 4));
@@ -313,12 +320,12 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
       const int slot = (int)(it % NS);
       mbar_wait(&full[slot], (uint32_t)((it / NS) & 1));
       const int j0 = c * (kUmKC / 4), nj = min(kUmKC / 4, ksteps - j0);
-      const uint32_t base = sbase + (uint32_t)(slot * kUmStageBytes);
+      const uint32_t base = sbase + (uint32_t)(slot * kUmStageBytes + qd * kUmQuadBytes);
       // own k-steps of the chunk: jj = kpart, kpart + KS, ... (two accumulator sets; issuing
       // the whole chunk's fragment loads first measured 7-14% slower)
 #pragma unroll 2
       for (int jj = kpart; jj < nj; jj += 2 * KS) {
-        const uint32_t a0 = base + 2048u * (uint32_t)jj;
+        const uint32_t a0 = base + 1024u * (uint32_t)jj;
         const double2 x0 = lds128(a0 + uoff0), x1 = lds128(a0 + uoff1);
         const double bv = lds64(cfb + (uint32_t)((j0 + jj) * NT * 256));
         dmma(d[0][0], d[0][1], x0.x, bv);
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
         dmma(d[3][0], d[3][1], x1.y, bv);
         const int j2 = jj + KS;
         if (j2 < nj) {
-          const uint32_t a2 = base + 2048u * (uint32_t)j2;
+          const uint32_t a2 = base + 1024u * (uint32_t)j2;
           const double2 y0 = lds128(a2 + uoff0), y1 = lds128(a2 + uoff1);
           const double bw = lds64(cfb + (uint32_t)((j0 + j2) * NT * 256));
           dmma(d2[0][0], d2[0][1], y0.x, bw);
