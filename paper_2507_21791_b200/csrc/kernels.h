@@ -141,8 +141,10 @@ struct alignas(64) UpdTmaParams {
   const double* srcB; long ld_srcB; double* dstB; long ld_dstB;
   const double* CB; long ldcb; const double* TB;
   const DevStatus* status;
+  double* coef_ws;     // >= update_tma_coef_doubles(s, kp): the packed coefficient fragments
 };
 cudaError_t update_tma_launch(UpdTmaParams& p, int num_sms, cudaStream_t st, int* launches);
+size_t update_tma_coef_doubles(int s, int kp);
 int update_tma_max_kp(int s);
 size_t update_tma_smem_bytes(int s, int kp, int stages);
 

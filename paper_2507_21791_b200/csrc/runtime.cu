@@ -303,6 +303,7 @@ struct bgs_ctx {
   HBuf hx, hq;                           // pinned mirrors for pageable caller buffers
   DBuf partial, G, scolA, scolB, sdiag, ydiag, save, r1, r2, rtop, R, status;
   DBuf tsqr_ws, tsqr_bounds, roots, roots_all, cross_ws, cross_m, metrics;
+  DBuf coefws;  // K2m: the update coefficients packed in DMMA-fragment order
   std::vector<DBuf> sx, sq;  // per-shard device buffers of the host-API path
   std::vector<DBuf> rscr;    // per-shard right-operand scratch of chunked Grams
   DBuf ticket;               // last-CTA ticket of the merged reduce + step kernel
@@ -323,7 +324,7 @@ struct bgs_ctx {
   std::vector<void*> buf_signature() const {
     return {partial.p, G.p, scolA.p, scolB.p, sdiag.p, ydiag.p, save.p, r1.p, r2.p, rtop.p, R.p,
             status.p, tsqr_ws.p, tsqr_bounds.p, roots.p, roots_all.p, cross_ws.p, cross_m.p,
-            ticket.p, metrics.p};
+            ticket.p, metrics.p, coefws.p};
   }
   int launches = 0;
   // live profiler: event pairs per launch, resolved after the stream syncs
@@ -374,6 +375,7 @@ struct bgs_ctx {
     for (auto& b : sx) b.release();
     for (auto& b : rscr) b.release();
     ticket.release();
+    coefws.release();
     for (auto& b : sq) b.release();
     for (auto& p : pending) {
       event_pool.push_back(p.a);
@@ -1167,6 +1169,8 @@ class Runner {
           q.has_b = u.has_b;
           q.cb_has_a = last ? u.cb_has_a : 0;
           q.status = status;
+          c->coefws.ensure(update_tma_coef_doubles((int)s, q.kp) * sizeof(double) + 64);
+          q.coef_ws = c->coefws.d();
           if (u.has_a) {
             q.srcA = c0 > 0 ? p.dstA : p.srcA; q.ld_srcA = c0 > 0 ? p.ld_dstA : p.ld_srcA;
             q.dstA = p.dstA; q.ld_dstA = p.ld_dstA;

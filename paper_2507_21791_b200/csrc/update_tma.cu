@@ -1,29 +1,28 @@
-// update_tma.cu — K2m: the block update for s = 8 / 16 with the prefix streamed by TMA.
+// update_tma.cu — K2m: the block update for s = 5..16 with the prefix streamed by TMA.
 //
 // Same algebra and call sites as K2 (update.cu; local_axpy_block + scale_right_block,
 // dist_block.cpp:90-117, bcgs.cpp:329-331, 346-359, 151-160):
 //   A = (srcA - Qp CA) TA^{-1},  B = (srcB - Qp CB[0:kp] - A CB[kp:kp+s]) TB^{-1}
 // At s >= 8 K2t (update.cu) fetched its DMMA A fragments with per-lane global loads and ran
-// latency-bound at 0.3-0.45 of the roofline (ncu: 20% occupancy, 32% / 20% DRAM at
-// s = 8 / 16, profiles/r02_ncu_k2t.md).  Here:
-//  * a persistent CTA per SM walks 64-row blocks of its shard; the prefix Q[:, 0:kp] of a
-//    block streams through a ring of k-chunk stages (64 rows x 32 columns as two 32-row
-//    quads, 3-D TMA boxes {16, 2, w}: 256-byte runs per column, SWIZZLE_128B; as many 16 KB stages as shared
-//    memory holds next to the coefficients), one producer thread;
-//  * the coefficients [CA | CB] (kp x 2S) sit in shared memory in DMMA-fragment order for
-//    the whole kernel;
-//  * 8 DMMA warps: warp w owns n-tile w % NT of [CA | CB] (NT = 2S / 8), 32-row quad
-//    (w / NT) % 2 and k-steps j = w / (2 NT) (mod KS = 8 / (2 NT)) of every chunk (K12c's
-//    conflict-free fragment scheme: two LDS.128 give a lane its 4 rows of a k-step);
-//  * the KS partial products of a block go to one of four shared scratch buffers (one slice
-//    per k-part), and one of four epilogue warps (round-robin over blocks, so the
-//    epilogues overlap the DMMAs of the next blocks) applies the block's factors: lane r
-//    owns rows r and 32 + r, sums the slices in k-part order and forms
-//    [A | B] = [srcA - D_A | srcB - D_B] M with K12c's explicit 2S x 2S factor
-//    matrix M (independent FMAs instead of K2's serial back-substitution chains, which
-//    made K2t's epilogue latency-bound at s = 16).
-// Bytes per row: 8 (kp + 2s) read + 8 (2s) written, as K2.  s = 8 is HBM-bound (AI 4),
-// s = 16 fp64-tensor-bound (AI 8).
+// latency-bound at 0.3-0.45 of the roofline (profiles/r02_ncu_k2t.md).  Here:
+//  * a persistent CTA per SM walks 128-row blocks of its shard; the prefix Q[:, 0:kp] of a
+//    block streams through a ring of k-chunk stages: 128 rows x 32 columns as four 32-row
+//    quads (3-D TMA boxes {16, 2, w}: 256-byte runs per column, SWIZZLE_128B, K12c's
+//    conflict-free fragment layout) FOLLOWED BY THE CHUNK'S COEFFICIENTS, already in
+//    DMMA-fragment order (one 1-D bulk copy from a buffer a small pack kernel fills once per
+//    launch).  The first K2m kept all kp x 2S coefficients in shared memory (102 KB at
+//    kp = 400, s = 16), which left room for neither a wider warp tile nor long prefixes;
+//  * 8 DMMA warps, each a 32-row quad x TWO n-tiles of [CA | CB] (8 accumulators: 8 DMMAs
+//    per 2 LDS.128 + 2 LDS.64; one n-tile per warp was shared-memory bound at s = 16: ncu
+//    79% of the shared pipe, DMMA pipe 48%): warp w = quad w % 4, and w / 4 selects the
+//    n-tile pair (s > 8: NT = 4) or the k-part (s <= 8: NT = 2, the k-steps split in two);
+//  * the products of a block go to one of two shared scratch buffers (one slice per k-part)
+//    and four epilogue warps, one per quad (lane r owns row 32 e + r), apply the block's
+//    factors while the DMMA warps run the next block: z = src - D, then
+//    [A | B] = [zA | zB] M with K12c's explicit 2S x 2S factor matrix M (independent FMAs
+//    instead of K2's serial back-substitution chains).
+// Bytes per row: 8 (kp + 2s) read + 8 (2s) written, as K2 (+ the coefficients once per block,
+// from L2).  s = 8 is HBM-bound (AI 4), s = 16 fp64-tensor-bound (AI 8).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -31,33 +30,38 @@ namespace bgs {
 
 namespace {
 constexpr int kUmWarps = 8;                          // DMMA warps
-constexpr int kUmEpi = 4;                            // epilogue warps (round-robin blocks)
+constexpr int kUmEpi = 4;                            // epilogue warps (one per quad)
 constexpr int kUmProd = kUmWarps + kUmEpi;           // producer warp index
 constexpr int kUmThreads = 32 * (kUmWarps + kUmEpi + 1);
-constexpr int kUmRows = 64;                          // rows per block (two 32-row quads)
+constexpr int kUmQuads = 4;                          // 32-row quads per block
+constexpr int kUmRows = 32 * kUmQuads;               // rows per block
 constexpr int kUmKC = 32;                            // prefix columns per stage
-constexpr int kUmStageBytes = kUmKC * kUmRows * 8;   // 16 KB
-constexpr int kUmQuadBytes = kUmKC * 32 * 8;         // a stage is two 32-row quads, quad-major
-constexpr int kUmStagesMax = 8;  // ring depth: as many 16 KB stages as fit (>= 3)
-constexpr int kUmBufs = kUmEpi;                      // D scratch buffers (one per epilogue warp)
+constexpr int kUmTileBytes = kUmKC * kUmRows * 8;    // 32 KB
+constexpr int kUmQuadBytes = kUmKC * 32 * 8;         // 8 KB
+constexpr int kUmNTW = 2;                            // n-tiles per DMMA warp
+constexpr int kUmStagesMax = 6;
+constexpr int kUmBufs = 2;                           // D scratch buffers (alternate blocks)
 constexpr int kUmSmemMax = 232448 - 1024;
 
 __host__ __device__ constexpr int um_nt(int S) { return 2 * S / 8; }
-// warp w: n-tile w % NT, quad (w / NT) % 2, k-part w / (2 NT) of KS = 8 / (2 NT)
-__host__ __device__ constexpr int um_ks(int S) { return kUmWarps / (2 * um_nt(S)); }
-// per-block scratch [KS k-parts][64 rows][2S + 1]; the epilogue sums the k-parts in order
-// (s = 16 has KS = 1: every warp owns whole (quad, n-tile) products)
-__host__ __device__ constexpr bool um_sliced(int S) { return um_ks(S) > 1; }
-__host__ __device__ constexpr int um_scratch_doubles(int S) {
-  return um_ks(S) * kUmRows * (2 * S + 1);
-}
+// k-parts: the 8 warps are 4 quads x (NT / 2 n-tile pairs) x KS
+__host__ __device__ constexpr int um_ks(int S) { return kUmWarps / (kUmQuads * (um_nt(S) / kUmNTW)); }
+__host__ __device__ constexpr int um_coef_chunk_bytes(int S) { return (kUmKC / 4) * um_nt(S) * 32 * 8; }
+__host__ __device__ constexpr int um_stage_bytes(int S) { return kUmTileBytes + um_coef_chunk_bytes(S); }
+// per-block scratch [KS k-parts][128 rows][2S + 1]; the epilogue sums the k-parts in order
+__host__ __device__ constexpr int um_scratch_doubles(int S) { return um_ks(S) * kUmRows * (2 * S + 1); }
 
 }  // namespace
 
-size_t update_tma_smem_bytes(int s, int kp, int stages) {
+size_t update_tma_coef_doubles(int s, int kp) {
   const int S = s <= 8 ? 8 : 16;
-  const size_t coef = (size_t)((kp + 3) / 4) * um_nt(S) * 32 * sizeof(double);
-  return 1024 + (size_t)stages * kUmStageBytes + coef +
+  return (size_t)((kp + 3) / 4) * um_nt(S) * 32;
+}
+
+size_t update_tma_smem_bytes(int s, int kp, int stages) {
+  (void)kp;
+  const int S = s <= 8 ? 8 : 16;
+  return 1024 + (size_t)stages * um_stage_bytes(S) +
          (size_t)kUmBufs * um_scratch_doubles(S) * sizeof(double) +
          (size_t)6 * S * S * sizeof(double) +
          (2 * kUmStagesMax + 2 * kUmBufs) * sizeof(uint64_t) + 64;
@@ -70,16 +74,32 @@ static int um_stages(int s, int kp) {
 }
 
 int update_tma_max_kp(int s) {
-  int best = 0;
-  for (int kp = 8; kp <= 4096; kp += 8)
-    if (um_stages(s, kp) >= 3) best = kp;
-  return best;
+  return um_stages(s, 8) >= 3 ? 1 << 20 : 0;  // (the coefficients stream: no panel limit)
+}
+
+// coefficient fragments: lane (i, kk) of n-tile t, k-step j holds C[4j + kk][8t + i]
+template <int S, bool HA, bool HB>
+__global__ void um_pack_kernel(const UpdTmaParams p) {
+  constexpr int NT = um_nt(S);
+  const int total = (p.kp / 4) * NT * 32;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int l = idx & 31, t = (idx >> 5) % NT, j = (idx >> 5) / NT;
+    const int c = 4 * j + (l & 3), n = 8 * t + (l >> 2);
+    double v = 0.0;
+    if (n < S) {
+      if (HA && n < p.s) v = p.CA[c + (size_t)n * p.ldca];
+    } else if (HB && n - S < p.s) {
+      v = p.CB[c + (size_t)(n - S) * p.ldcb];
+    }
+    p.coef_ws[idx] = v;
+  }
 }
 
 template <int S, bool HA, bool HB>
 __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_constant__ UpdTmaParams p) {
   constexpr int NT = um_nt(S), KS = um_ks(S);
   constexpr int LDD = 2 * S + 1;
+  constexpr int kStage = um_stage_bytes(S);
   if (p.status && status_bad(p.status)) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -88,8 +108,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   const int ksteps = kp / 4;                       // kp is a multiple of 8 here
   const int nchunk = (kp + kUmKC - 1) / kUmKC;
   const int NS = p.stages;
-  double* coef = reinterpret_cast<double*>(smem + (size_t)NS * kUmStageBytes);
-  double* scr = coef + (size_t)ksteps * NT * 32;   // [kUmBufs][32][LDD]
+  double* scr = reinterpret_cast<double*>(smem + (size_t)NS * kStage);  // [kUmBufs][KS][128][LDD]
   double* ta = scr + (size_t)kUmBufs * um_scratch_doubles(S);  // S x S each (col-major)
   double* tb = ta + S * S;
   double* tai = tb + S * S;                        // TA^{-1}
@@ -121,21 +140,9 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
     }
     for (int i = 0; i < kUmBufs; ++i) {
       mbar_init(&dfull[i], kUmWarps);
-      mbar_init(&dempty[i], 1);
+      mbar_init(&dempty[i], kUmEpi);
     }
     fence_mbar_init();
-  }
-  // coefficient fragments: lane (i, kk) of n-tile t, k-step j holds C[4j + kk][8t + i]
-  for (int idx = threadIdx.x; idx < ksteps * NT * 32; idx += blockDim.x) {
-    const int l = idx & 31, t = (idx >> 5) % NT, j = (idx >> 5) / NT;
-    const int c = 4 * j + (l & 3), n = 8 * t + (l >> 2);
-    double v = 0.0;
-    if (n < S) {
-      if (HA && n < s) v = p.CA[c + (size_t)n * p.ldca];
-    } else if (HB && n - S < s) {
-      v = p.CB[c + (size_t)(n - S) * p.ldcb];
-    }
-    coef[idx] = v;
   }
   for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {
     const int i = idx % S, j = idx / S;
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   __syncthreads();
 
   if (warp == kUmProd) {
-    // ---------------- producer: k-chunk stages of every block ----------------
+    // ---------------- producer: k-chunk stages (tile quads + coefficients) of every block ----------------
     if (lane == 0) {
       for (int i = 0; i < 5; ++i) prefetch_tmap(&p.map[i]);
       long it = 0;
@@ -188,17 +195,19 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
           const int slot = (int)(it % NS);
           if (it >= NS) mbar_wait(&empty[slot], (uint32_t)(((it / NS) - 1) & 1));
           const int c0 = c * kUmKC, w = min(kUmKC, kp - c0);
-          mbar_arrive_expect_tx(&full[slot], (uint32_t)(w * kUmRows * 8));
-          unsigned char* dst = smem + (size_t)slot * kUmStageBytes;
+          const uint32_t cbytes = (uint32_t)((w / 4) * NT * 32 * 8);
+          mbar_arrive_expect_tx(&full[slot], (uint32_t)(w * kUmRows * 8) + cbytes);
+          unsigned char* dst = smem + (size_t)slot * kStage;
+          bulk_load_1d(dst + kUmTileBytes, p.coef_ws + (size_t)(c0 / 4) * NT * 32, cbytes, &full[slot]);
           int done = 0;
           while (done < w) {  // greedy boxes {16, 2, 32 / 16 / 8}, one per 32-row quad
             const int left = w - done;
             const int wi = left >= 32 ? 2 : left >= 16 ? 3 : 4;
             BGS_DCHECK(done + (128 >> wi) <= kUmKC, "k2m: TMA box past the stage");
 #pragma unroll
-            for (int qd = 0; qd < 2; ++qd)
+            for (int qd = 0; qd < kUmQuads; ++qd)
               tma_load_3d(dst + (size_t)qd * kUmQuadBytes + (size_t)done * 256, &p.map[wi],
-                          &full[slot], 0, (int)(4 * b + 2 * qd), p.col0 + c0 + done);
+                          &full[slot], 0, (int)(2 * kUmQuads * b + 2 * qd), p.col0 + c0 + done);
             done += 128 >> wi;
           }
         }
@@ -208,99 +217,89 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   }
 
   if (warp >= kUmWarps) {
-    // ---------------- epilogue warps: block b on warp kUmWarps + (b - b0) % kUmEpi ----------------
+    // ---------------- epilogue warps: warp e takes quad e (row 32 e + lane) of every block ----------------
     const int e = warp - kUmWarps;
-    long u = 0;  // this warp's blocks so far
-    for (long b = b0 + e; b < b1; b += kUmEpi, ++u) {
-      double* zb0 = scr + (size_t)e * um_scratch_doubles(S);
-      // the sources of both rows of this lane do not depend on the contraction: loaded
-      // before the wait
-      double za[2][S], zb[2][S];
+    long u = 0;  // blocks so far
+    for (long b = b0; b < b1; ++b, ++u) {
+      const int buf = (int)(u % kUmBufs);
+      double* zb0 = scr + (size_t)buf * um_scratch_doubles(S);
+      const long row = b * kUmRows + 32 * e + lane;
+      const bool live = row < p.n_rows;
+      // the sources of this lane's row do not depend on the contraction: loaded before the wait
+      double za[S], zb[S];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const long row = b * kUmRows + 32 * h + lane;
-        const bool live = row < p.n_rows;
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-          za[h][j] = (HA && live && j < s) ? p.srcA[row + (size_t)j * p.ld_srcA] : 0.0;
-          zb[h][j] = (HB && live && j < s) ? p.srcB[row + (size_t)j * p.ld_srcB] : 0.0;
-        }
+      for (int j = 0; j < S; ++j) {
+        za[j] = (HA && live && j < s) ? p.srcA[row + (size_t)j * p.ld_srcA] : 0.0;
+        zb[j] = (HB && live && j < s) ? p.srcB[row + (size_t)j * p.ld_srcB] : 0.0;
       }
-      mbar_wait(&dfull[e], (uint32_t)(u & 1));
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const long row = b * kUmRows + 32 * h + lane;
-        const bool live = row < p.n_rows;
-        // z = src - D, in place in this row of the scratch (odd stride: conflict-free)
-        double* zr = zb0 + (size_t)(32 * h + lane) * LDD;
+      mbar_wait(&dfull[buf], (uint32_t)((u / kUmBufs) & 1));
+      // z = src - D, in place in this row of the scratch (odd stride: conflict-free)
+      double* zr = zb0 + (size_t)(32 * e + lane) * LDD;
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-          double da = zr[j], db = zr[S + j];
-          if (um_sliced(S)) {
+      for (int j = 0; j < S; ++j) {
+        double da = zr[j], db = zr[S + j];
+        if (KS > 1) {
 #pragma unroll
-            for (int k2 = 1; k2 < KS; ++k2) {  // k-part order
-              da += zr[(size_t)k2 * kUmRows * LDD + j];
-              db += zr[(size_t)k2 * kUmRows * LDD + S + j];
-            }
+          for (int k2 = 1; k2 < KS; ++k2) {  // k-part order
+            da += zr[(size_t)k2 * kUmRows * LDD + j];
+            db += zr[(size_t)k2 * kUmRows * LDD + S + j];
           }
-          if (HA) zr[j] = za[h][j] - da;
-          if (HB) zr[S + j] = zb[h][j] - db;
         }
-        if (HA) {
-          double a[S];
+        if (HA) zr[j] = za[j] - da;
+        if (HB) zr[S + j] = zb[j] - db;
+      }
+      if (HA) {
+        double a[S];
 #pragma unroll
-          for (int j = 0; j < S; ++j) a[j] = 0.0;
+        for (int j = 0; j < S; ++j) a[j] = 0.0;
 #pragma unroll 1
-          for (int l = 0; l < S; ++l) {  // (TA^{-1} is upper triangular with exact zeros)
-            const double z = zr[l];
+        for (int l = 0; l < S; ++l) {  // (TA^{-1} is upper triangular with exact zeros)
+          const double z = zr[l];
 #pragma unroll
-            for (int j = 0; j < S; ++j) a[j] = fma(z, tai[l + j * S], a[j]);
-          }
-          if (live)
-#pragma unroll
-            for (int j = 0; j < S; ++j)
-              if (j < s) p.dstA[row + (size_t)j * p.ld_dstA] = a[j];
+          for (int j = 0; j < S; ++j) a[j] = fma(z, tai[l + j * S], a[j]);
         }
-        if (HB) {
-          double bb[S];
+        if (live)
 #pragma unroll
-          for (int j = 0; j < S; ++j) bb[j] = 0.0;
-          if (HA && p.cb_has_a) {
-#pragma unroll 1
-            for (int l = 0; l < S; ++l) {
-              const double z = zr[l];
+          for (int j = 0; j < S; ++j)
+            if (j < s) p.dstA[row + (size_t)j * p.ld_dstA] = a[j];
+      }
+      if (HB) {
+        double bb[S];
 #pragma unroll
-              for (int j = 0; j < S; ++j) bb[j] = fma(z, mab[l + j * S], bb[j]);
-            }
-          }
+        for (int j = 0; j < S; ++j) bb[j] = 0.0;
+        if (HA && p.cb_has_a) {
 #pragma unroll 1
           for (int l = 0; l < S; ++l) {
-            const double z = zr[S + l];
+            const double z = zr[l];
 #pragma unroll
-            for (int j = 0; j < S; ++j) bb[j] = fma(z, tbi[l + j * S], bb[j]);
+            for (int j = 0; j < S; ++j) bb[j] = fma(z, mab[l + j * S], bb[j]);
           }
-          if (live)
-#pragma unroll
-            for (int j = 0; j < S; ++j)
-              if (j < s) p.dstB[row + (size_t)j * p.ld_dstB] = bb[j];
         }
+#pragma unroll 1
+        for (int l = 0; l < S; ++l) {
+          const double z = zr[S + l];
+#pragma unroll
+          for (int j = 0; j < S; ++j) bb[j] = fma(z, tbi[l + j * S], bb[j]);
+        }
+        if (live)
+#pragma unroll
+          for (int j = 0; j < S; ++j)
+            if (j < s) p.dstB[row + (size_t)j * p.ld_dstB] = bb[j];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&dempty[e]);  // the scratch is free again
+      if (lane == 0) mbar_arrive(&dempty[buf]);  // (all four quads: the scratch is free again)
     }
     return;
   }
 
   // ---------------- DMMA warps ----------------
-  const int t = warp % NT, qd = (warp / NT) & 1, kpart = warp / (2 * NT);
+  const int qd = warp % kUmQuads, g2 = warp / kUmQuads;
+  const int tp = NT > kUmNTW ? g2 : 0;         // n-tile pair of this warp
+  const int kpart = NT > kUmNTW ? 0 : g2;      // or its k-part
   const int ii = lane >> 2, kk = lane & 3;
-  // m-tile q of quad qd, row index i is block row 32 qd + 4 f(i) + q with
-  // f(i) = (i >> 1) + 4 (i & 1): two LDS.128 give lane (i, kk) its 4 rows of k-step column
-  // 4j + kk (k12.cu's conflict-free scheme on K12c's {16, 2, w} quad layout: line 2c + h, so
-  // the four kk of a quarter-warp hit four distinct 16-byte chunk positions.  The first K2m
-  // kept the 64 rows of a column together ({16, 4, w}: line 4c + h), where kk = 0, 2 and
-  // 1, 3 collide: every fragment load took two wavefronts; ncu showed the shared pipe at
-  // 79% and the DMMA pipe at 48% at s = 16)
+  // m-tile q of the quad, row index i is quad row 4 f(i) + q with f(i) = (i >> 1) + 4 (i & 1):
+  // two LDS.128 give lane (i, kk) its 4 rows of k-step column 4j + kk (K12c's conflict-free
+  // scheme on the {16, 2, w} quad layout: line 2c + h)
   uint32_t uoff0, uoff1;
   {
     const int line = 2 * kk + (ii & 1);
@@ -310,53 +309,52 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   }
   const int f = (ii >> 1) + 4 * (ii & 1);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t cfb = smem_u32(coef) + (uint32_t)((t * 32 + lane) * 8);
+  // this lane's coefficient of n-tile 2 tp + n2, local k-step jj: chunk + ((jj NT + t) 32 + lane) 8
+  const uint32_t cfo = (uint32_t)(kUmTileBytes + ((kUmNTW * tp) * 32 + lane) * 8);
   long it = 0;
   for (long b = b0; b < b1; ++b) {
-    double d[4][2], d2[4][2];
+    double d[4][kUmNTW][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) d[q][0] = d[q][1] = d2[q][0] = d2[q][1] = 0.0;
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int n2 = 0; n2 < kUmNTW; ++n2) d[q][n2][0] = d[q][n2][1] = 0.0;
     for (int c = 0; c < nchunk; ++c, ++it) {
       const int slot = (int)(it % NS);
       mbar_wait(&full[slot], (uint32_t)((it / NS) & 1));
       const int j0 = c * (kUmKC / 4), nj = min(kUmKC / 4, ksteps - j0);
-      const uint32_t base = sbase + (uint32_t)(slot * kUmStageBytes + qd * kUmQuadBytes);
-      // own k-steps of the chunk: jj = kpart, kpart + KS, ... (two accumulator sets; issuing
-      // the whole chunk's fragment loads first measured 7-14% slower)
+      const uint32_t stg = sbase + (uint32_t)(slot * kStage);
+      const uint32_t base = stg + (uint32_t)(qd * kUmQuadBytes);
 #pragma unroll 2
-      for (int jj = kpart; jj < nj; jj += 2 * KS) {
+      for (int jj = kpart; jj < nj; jj += KS) {
         const uint32_t a0 = base + 1024u * (uint32_t)jj;
         const double2 x0 = lds128(a0 + uoff0), x1 = lds128(a0 + uoff1);
-        const double bv = lds64(cfb + (uint32_t)((j0 + jj) * NT * 256));
-        dmma(d[0][0], d[0][1], x0.x, bv);
-        dmma(d[1][0], d[1][1], x0.y, bv);
-        dmma(d[2][0], d[2][1], x1.x, bv);
-        dmma(d[3][0], d[3][1], x1.y, bv);
-        const int j2 = jj + KS;
-        if (j2 < nj) {
-          const uint32_t a2 = base + 1024u * (uint32_t)j2;
-          const double2 y0 = lds128(a2 + uoff0), y1 = lds128(a2 + uoff1);
-          const double bw = lds64(cfb + (uint32_t)((j0 + j2) * NT * 256));
-          dmma(d2[0][0], d2[0][1], y0.x, bw);
-          dmma(d2[1][0], d2[1][1], y0.y, bw);
-          dmma(d2[2][0], d2[2][1], y1.x, bw);
-          dmma(d2[3][0], d2[3][1], y1.y, bw);
-        }
+        const uint32_t cf = stg + cfo + (uint32_t)(jj * NT * 256);
+        const double bv0 = lds64(cf), bv1 = lds64(cf + 256u);
+        dmma(d[0][0][0], d[0][0][1], x0.x, bv0);
+        dmma(d[1][0][0], d[1][0][1], x0.y, bv0);
+        dmma(d[2][0][0], d[2][0][1], x1.x, bv0);
+        dmma(d[3][0][0], d[3][0][1], x1.y, bv0);
+        dmma(d[0][1][0], d[0][1][1], x0.x, bv1);
+        dmma(d[1][1][0], d[1][1][1], x0.y, bv1);
+        dmma(d[2][1][0], d[2][1][1], x1.x, bv1);
+        dmma(d[3][1][0], d[3][1][1], x1.y, bv1);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
-    // this warp's product -> scratch[(b - b0) % kUmBufs][kpart][row][8t + 2kk + e]
+    // this warp's product -> scratch[(b - b0) % kUmBufs][kpart][row][8 t + 2 kk + e]
     const long ub = b - b0;
     const int e = (int)(ub % kUmBufs);
     if (ub >= kUmBufs) mbar_wait(&dempty[e], (uint32_t)((ub / kUmBufs - 1) & 1));
     double* sl = scr + (size_t)e * um_scratch_doubles(S) + (size_t)kpart * kUmRows * LDD;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double* rp = sl + (size_t)(32 * qd + 4 * f + q) * LDD + 8 * t + 2 * kk;
-      rp[0] = d[q][0] + d2[q][0];
-      rp[1] = d[q][1] + d2[q][1];
-    }
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int n2 = 0; n2 < kUmNTW; ++n2) {
+        double* rp = sl + (size_t)(32 * qd + 4 * f + q) * LDD + 8 * (kUmNTW * tp + n2) + 2 * kk;
+        rp[0] = d[q][n2][0];
+        rp[1] = d[q][n2][1];
+      }
     __syncwarp();
     if (lane == 0) mbar_arrive(&dfull[e]);
   }
@@ -364,6 +362,8 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
 
 template <int S, bool HA, bool HB>
 static cudaError_t launch_um(const UpdTmaParams& p, int grid, cudaStream_t st) {
+  const int total = (p.kp / 4) * um_nt(S) * 32;
+  um_pack_kernel<S, HA, HB><<<std::max(1, std::min(64, (total + 255) / 256)), 256, 0, st>>>(p);
   auto k = update_tma_kernel<S, HA, HB>;
   const size_t smem = update_tma_smem_bytes(S, p.kp, p.stages);
   cudaError_t e = ensure_smem(k, smem);
@@ -373,13 +373,13 @@ static cudaError_t launch_um(const UpdTmaParams& p, int grid, cudaStream_t st) {
 }
 
 cudaError_t update_tma_launch(UpdTmaParams& p, int num_sms, cudaStream_t st, int* launches) {
-  if (p.s < 5 || p.s > 16 || p.kp < 8 || p.kp % 8 || p.kp > update_tma_max_kp(p.s))
-    return cudaErrorInvalidValue;
+  if (p.s < 5 || p.s > 16 || p.kp < 8 || p.kp % 8 || !p.coef_ws) return cudaErrorInvalidValue;
   p.total_blocks = (p.n_rows + kUmRows - 1) / kUmRows;
   p.stages = um_stages(p.s, p.kp);
+  if (p.stages < 3) return cudaErrorInvalidValue;
   if (p.total_blocks < 1) return cudaSuccess;
   const int grid = (int)std::min<long>(num_sms, p.total_blocks);
-  if (launches) *launches += 1;
+  if (launches) *launches += 2;
   const bool S8 = p.s <= 8;
   if (p.has_a && p.has_b)
     return S8 ? launch_um<8, true, true>(p, grid, st) : launch_um<16, true, true>(p, grid, st);
