@@ -6,8 +6,9 @@ names = ["wait", "update", "exchange", "epilogue", "gram", "tail"]
 for kp in kps:
     env = dict(os.environ, BGS_TILE_PROF="1", BGS_PROF_MINKP=str(kp), BGS_PROF_MAXKP=str(kp),
                BGS_TIMELINE="1")
+    extra = ["--m", os.environ["M"]] if os.environ.get("M") else []
     out = subprocess.run([sys.executable, "bench.py", "--steps", "1", "--warmup", "1", "--no-cpu",
-                          "--no-e2e", "--no-verify"], env=env, capture_output=True, text=True)
+                          "--no-e2e", "--no-verify"] + extra, env=env, capture_output=True, text=True)
     rows = {}
     for l in out.stderr.splitlines():
         m = re.match(r"\[k12c timeline\] g (\d) j +(\d+): (.*)", l)
