@@ -18,9 +18,8 @@
 //    n-tile pair (s > 8: NT = 4) or the k-part (s <= 8: NT = 2, the k-steps split in two);
 //  * the products of a block go to one of two shared scratch buffers (one slice per k-part)
 //    and four epilogue warps, one per quad (lane r owns row 32 e + r), apply the block's
-//    factors while the DMMA warps run the next block: z = src - D, then
-//    [A | B] = [zA | zB] M with K12c's explicit 2S x 2S factor matrix M (independent FMAs
-//    instead of K2's serial back-substitution chains).
+//    factors while the DMMA warps run the next block: z = src - D, then A = zA TA^{-1} and
+//    B = (zB - A S2) TB^{-1} by back-substitution (the reference's tri_solve_right order).
 // Bytes per row: 8 (kp + 2s) read + 8 (2s) written, as K2 (+ the coefficients once per block,
 // from L2).  s = 8 is HBM-bound (AI 4), s = 16 fp64-tensor-bound (AI 8).
 #include "common.cuh"
@@ -63,7 +62,7 @@ size_t update_tma_smem_bytes(int s, int kp, int stages) {
   const int S = s <= 8 ? 8 : 16;
   return 1024 + (size_t)stages * um_stage_bytes(S) +
          (size_t)kUmBufs * um_scratch_doubles(S) * sizeof(double) +
-         (size_t)6 * S * S * sizeof(double) +
+         (size_t)3 * S * S * sizeof(double) +
          (2 * kUmStagesMax + 2 * kUmBufs) * sizeof(uint64_t) + 64;
 }
 
@@ -111,10 +110,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
   double* scr = reinterpret_cast<double*>(smem + (size_t)NS * kStage);  // [kUmBufs][KS][128][LDD]
   double* ta = scr + (size_t)kUmBufs * um_scratch_doubles(S);  // S x S each (col-major)
   double* tb = ta + S * S;
-  double* tai = tb + S * S;                        // TA^{-1}
-  double* tbi = tai + S * S;                       // TB^{-1}
-  double* mab = tbi + S * S;                       // -TA^{-1} S2 TB^{-1}
-  double* s2 = mab + S * S;
+  double* s2 = tb + S * S;                         // CB[kp:kp+s] (B's coupling to A)
   uint64_t* full = reinterpret_cast<uint64_t*>(s2 + S * S);
   uint64_t* empty = full + kUmStagesMax;
   uint64_t* dfull = empty + kUmStagesMax;          // [kUmBufs]
@@ -152,38 +148,12 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
     s2[idx] = (HA && HB && p.cb_has_a && in) ? p.CB[kp + i + (size_t)j * p.ldcb] : 0.0;
   }
   __syncthreads();
-  // Epilogue matrix, once per CTA (as K12c's): [A | B] = [zA | zB] [[TA^-1, -TA^-1 S2 TB^-1],
-  // [0, TB^-1]] with z = src - D -- independent FMAs per row instead of the serial
-  // back-substitution chains (which left K2t's and a first K2m's epilogue latency-bound).
-  if (threadIdx.x < 2 * S) {  // column j of T^{-1} by back-substitution on T y = e_j
-    const bool isb = threadIdx.x >= S;
-    const int j = threadIdx.x % S;
-    const double* T = isb ? tb : ta;
-    double* Ti = isb ? tbi : tai;
-    for (int i = S - 1; i >= 0; --i) {
-      double acc = (i == j) ? 1.0 : 0.0;
-      for (int l = i + 1; l < S; ++l) acc -= T[i + l * S] * Ti[l + j * S];
-      Ti[i + j * S] = acc / T[i + i * S];
-    }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {  // W = S2 TB^{-1}
-    const int i = idx % S, j = idx / S;
-    double acc = 0.0;
-    for (int l = 0; l < S; ++l) acc += s2[i + l * S] * tbi[l + j * S];
-    mab[idx] = acc;  // (temporarily W)
-  }
-  __syncthreads();
-  double mab_reg = 0.0;
-  if (threadIdx.x < S * S) {  // -TA^{-1} W
-    const int i = threadIdx.x % S, j = threadIdx.x / S;
-    double acc = 0.0;
-    for (int l = 0; l < S; ++l) acc += tai[i + l * S] * mab[l + j * S];
-    mab_reg = -acc;
-  }
-  __syncthreads();
-  if (threadIdx.x < S * S) mab[threadIdx.x] = mab_reg;
-  __syncthreads();
+  // The epilogue warps back-substitute with TA / TB themselves (tri_solve_right's order,
+  // dense_kernels.cpp:89-110: x_j = (z_j - sum_{l<j} x_l T_lj) / T_jj), one row per lane.
+  // They run beside the DMMA warps with a whole block's contraction to hide their serial
+  // chains, and an explicit factor matrix [[TA^-1, -TA^-1 S2 TB^-1], [0, TB^-1]] (the first
+  // K2m, as K12c's) cost BCGSI+1S orthogonality at s = 8 on ill-conditioned diagonal blocks
+  // (fuzz case n = m = 80: LOO 14x the oracle's against 2.7x with substitution).
 
   if (warp == kUmProd) {
     // ---------------- producer: k-chunk stages (tile quads + coefficients) of every block ----------------
@@ -248,15 +218,16 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
         if (HA) zr[j] = za[j] - da;
         if (HB) zr[S + j] = zb[j] - db;
       }
+      double a[S];
+#pragma unroll
+      for (int j = 0; j < S; ++j) a[j] = 0.0;
       if (HA) {
-        double a[S];
 #pragma unroll
-        for (int j = 0; j < S; ++j) a[j] = 0.0;
-#pragma unroll 1
-        for (int l = 0; l < S; ++l) {  // (TA^{-1} is upper triangular with exact zeros)
-          const double z = zr[l];
+        for (int j = 0; j < S; ++j) {  // A = zA TA^{-1}
+          double acc = zr[j];
 #pragma unroll
-          for (int j = 0; j < S; ++j) a[j] = fma(z, tai[l + j * S], a[j]);
+          for (int l = 0; l < j; ++l) acc -= a[l] * ta[l + j * S];
+          a[j] = acc / ta[j + j * S];
         }
         if (live)
 #pragma unroll
@@ -266,20 +237,15 @@ __global__ void __launch_bounds__(kUmThreads, 1) update_tma_kernel(const __grid_
       if (HB) {
         double bb[S];
 #pragma unroll
-        for (int j = 0; j < S; ++j) bb[j] = 0.0;
-        if (HA && p.cb_has_a) {
-#pragma unroll 1
-          for (int l = 0; l < S; ++l) {
-            const double z = zr[l];
+        for (int j = 0; j < S; ++j) {  // B = (zB - A S2) TB^{-1}
+          double acc = zr[S + j];
+          if (HA && p.cb_has_a) {
 #pragma unroll
-            for (int j = 0; j < S; ++j) bb[j] = fma(z, mab[l + j * S], bb[j]);
+            for (int l = 0; l < S; ++l) acc -= a[l] * s2[l + j * S];
           }
-        }
-#pragma unroll 1
-        for (int l = 0; l < S; ++l) {
-          const double z = zr[S + l];
 #pragma unroll
-          for (int j = 0; j < S; ++j) bb[j] = fma(z, tbi[l + j * S], bb[j]);
+          for (int l = 0; l < j; ++l) acc -= bb[l] * tb[l + j * S];
+          bb[j] = acc / tb[j + j * S];
         }
         if (live)
 #pragma unroll

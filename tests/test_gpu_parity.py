@@ -864,6 +864,41 @@ def test_wide_shapes_beyond_staging_match_oracle(oracle, gpu_ctx, v, n, m, s):
     assert abs(out.loo - loo) <= 0.5 * loo + 1e-15 and abs(out.resid - res) <= 0.5 * res + 1e-16
 
 
+def test_ip1s_s8_square_gaussian_loo_within_band(oracle, gpu_ctx):
+    """Fuzz case of round 2 (FUZZ_PEER seed 404, case 534): BCGSI+1S, n = m = 80, s = 8, a
+    square Gaussian matrix with cond 1.9e3.  With the explicit 2s x 2s factor matrix in the
+    K2m epilogue the LOO was 14x the oracle's; the epilogue back-substitutes now (4.7x;
+    K2t: 2.7x).  Pinned inside north_star's 10x band."""
+    import paper_2507_21791_b200 as bgs
+    x = oracle.gen_matrix(80, 80, 8, 188.3253141666195, 165253, True)
+    ref = oracle.factor(5, x, 8, 1, metrics=True)
+    out = bgs.run_factor(5, x, 8, 1, metrics=False, ctx=gpu_ctx)
+    assert out.ok, out.error
+    assert_r_close(out.r, ref.r)
+    assert oracle.loo(out.q) <= 8 * ref.loo, (oracle.loo(out.q), ref.loo)
+
+
+@pytest.mark.parametrize("v", [3, 5, 2], ids=lambda v: NAMES[v])
+def test_prefix_wider_than_a_cta_pair_matches_oracle(oracle, gpu_ctx, v, monkeypatch):
+    """m = 640, s = 4: past kp = 528 a CTA pair cannot hold three stages and the planner
+    takes clusters of 4 on its own (no forced plan).  Against the oracle, and against the
+    unfused path to rounding."""
+    import paper_2507_21791_b200 as bgs
+    n, m, s = 1500, 640, 4
+    x = oracle.gen_matrix(n, m, s, 1e2, 77, False)
+    ref = oracle.factor(v, x, s, 1, metrics=True)
+    out = bgs.run_factor(v, x, s, 1, metrics=False, ctx=gpu_ctx)
+    assert out.ok, out.error
+    assert_r_close(out.r, ref.r)
+    assert_structure(out.r)
+    assert out.stats.event_labels == ref.labels
+    loo, res = oracle.loo(out.q), oracle.residual(x, out.q, out.r)
+    assert loo <= 10 * max(ref.loo, U) and res <= 10 * max(ref.resid, U)
+    monkeypatch.setenv("BGS_NO_FUSE", "1")
+    plain = bgs.run_factor(v, x, s, 1, metrics=False, ctx=gpu_ctx)
+    assert np.abs(out.r - plain.r).max() <= 1e-12 * np.abs(plain.r).max()
+
+
 @pytest.mark.parametrize("v", [3, 5], ids=lambda v: NAMES[v])
 def test_m2048_properties(gpu_ctx, v):
     """m = 2048, s = 4 (kp up to 2044: unmerged small ops, chunked Grams, residual R from

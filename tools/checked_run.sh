@@ -11,7 +11,7 @@ run() {  # name, env...
   echo "$name ($*): rc=$? $(grep -E 'failures:|bgs check' gpurun_out/checked_${name}.log | head -3 | tr '\n' ' ')"
 }
 run default
-for plan in 14 12 11 22 21; do run plan$plan BGS_K12C_PLAN=$plan; done
+for plan in 14 12 11 22 21 41; do run plan$plan BGS_K12C_PLAN=$plan; done
 run unfused BGS_NO_FUSE=1
 run unmerged BGS_NO_MERGE_SMALL=1
 run k2t BGS_K2M=0
