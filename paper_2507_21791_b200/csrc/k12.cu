@@ -82,7 +82,7 @@ bool k12_plan(SplitParams& p) {
     const char* ke = getenv("BGS_K12C_KWMAX");
     const int kw_r1 = ke ? std::max(kKwMax, std::min(kKwMaxR1, atoi(ke))) : kKwMaxR1;
     const int kw_max = (cd.C == 1 && cd.R == 1) ? kw_r1 : kKwMax;
-    int kw_t = std::max(1, kw);
+    int kw_t = std::max(cd.C == 4 ? 8 : 1, kw);  // (cluster-of-4 instances start at KW 8)
     while (kw_t <= kw_max && mtw_for(kw_t, cd.R) < mtw) ++kw_t;
     if (kw_t > kw_max) continue;
     const char* me = getenv("BGS_K12C_MINS");  // experiments: minimum ring depth (default 3)
@@ -129,7 +129,7 @@ int k12_grid_cap(int C, int sms) {
   static int cached[2] = {0, 0};
   int& c = cached[C == 4 ? 0 : 1];
   if (!c) {
-    auto k = k12_kernel<13, mtw_for(13, 1), 1, false>;
+    auto k = k12_kernel<13, mtw_for(13, 1), 1, false, true>;
     const size_t smem = (size_t)kSmemOptin - kStaticSmem - 256;
     int n = 0;
     if (ensure_smem(k, smem) == cudaSuccess) {

@@ -102,7 +102,10 @@ __device__ __forceinline__ unsigned long long k12_gtime() {
 }
 #endif
 
-template <int KW, int MTW, int R, bool CT>
+// QUAD: the cluster-of-4 instances (their own template flag: the generic 4-way exchange in
+// the pair instances cost the CTA-pair steps 5%: 215 cycles more in the exchange phase and
+// registers in the epilogue).
+template <int KW, int MTW, int R, bool CT, bool QUAD = false>
 __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant__ SplitParams p) {
 #if defined(BGS_STEP_STAMPS) && !defined(BGS_K12_NO_STAMPS)
   const unsigned long long t_entry = k12_gtime();
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int nrk = p.cluster;   // CTAs per cluster: 1, 2 or 4
+  const int nrk = QUAD ? 4 : p.cluster;  // CTAs per cluster: 1, 2 (or 4: QUAD instances)
   const bool pair = nrk > 1;  // (a cluster splits the prefix columns over its CTAs)
   const int S = p.stages;
   const int chunk_bytes = p.slot_units * kUnitChunkBytes;
@@ -502,47 +505,70 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
         }
       }
       if (pair) {
-        // ---- exchange with the same warp of every peer rank (DSMEM); rank q's partial lands
-        // in source slot (q < r ? q : q - 1) of rank r ----
-        const int xb = g * 2 + (j & 1);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q >= nrk || q == (int)rank) continue;
-          const int src = (int)rank < q ? (int)rank : (int)rank - 1;
-          const uint32_t rbar = mapa_shared(xfull_local + (uint32_t)(xb * 8), (uint32_t)q);
+        if constexpr (QUAD) {
+          // ---- exchange with the same warp of every peer rank (DSMEM); rank q's partial lands
+          // in source slot (q < r ? q : q - 1) of rank r ----
+          const int xb = g * 2 + (j & 1);
+  #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q >= nrk || q == (int)rank) continue;
+            const int src = (int)rank < q ? (int)rank : (int)rank - 1;
+            const uint32_t rbar = mapa_shared(xfull_local + (uint32_t)(xb * 8), (uint32_t)q);
+  #pragma unroll
+            for (int ch = 0; ch < R; ++ch) {
+              const uint32_t dst = xb_local + (uint32_t)((((((xb * (nrk - 1) + src) * R + ch) * kGroupWarps + w) * 32 + lane) * 16));
+              st_async_v2f64(mapa_shared(dst, (uint32_t)q), D0[ch], D1[ch], rbar);
+            }
+          }
+          if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], (nrk - 1) * R * kGroupWarps * 32 * 16);
+          mbar_wait(&xfull[xb], (j >> 1) & 1);  // data and completion are both CTA-local
+          // every rank adds the partials in rank order 0, 1, ...: identical bits on all of them
+          // (two ranks: own + other, as IEEE addition commutes)
+  #pragma unroll
+          for (int ch = 0; ch < R; ++ch) {
+            double a0 = 0.0, a1 = 0.0;
+  #pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (q >= nrk) continue;
+              double2 v;
+              if (q == (int)rank) {
+                v = make_double2(D0[ch], D1[ch]);
+              } else {
+                const int src = q < (int)rank ? q : q - 1;
+                v = lds128(xb_local + (uint32_t)((((((xb * (nrk - 1) + src) * R + ch) * kGroupWarps + w) * 32 + lane) * 16)));
+              }
+              if (q == 0) {
+                a0 = v.x;
+                a1 = v.y;
+              } else {
+                a0 += v.x;
+                a1 += v.y;
+              }
+            }
+            D0[ch] = a0;
+            D1[ch] = a1;
+          }
+        } else {
+          // ---- exchange with the same warp of the peer rank (DSMEM) ----
+          const uint32_t peer = rank ^ 1u;
+          const int xb = g * 2 + (j & 1);
+          const uint32_t rbar = mapa_shared(xfull_local + (uint32_t)(xb * 8), peer);
 #pragma unroll
           for (int ch = 0; ch < R; ++ch) {
-            const uint32_t dst = xb_local + (uint32_t)((((((xb * (nrk - 1) + src) * R + ch) * kGroupWarps + w) * 32 + lane) * 16));
-            st_async_v2f64(mapa_shared(dst, (uint32_t)q), D0[ch], D1[ch], rbar);
+            const uint32_t mine =
+                xb_local + (uint32_t)((((xb * R + ch) * kGroupWarps + w) * 32 + lane) * 16);
+            st_async_v2f64(mapa_shared(mine, peer), D0[ch], D1[ch], rbar);
           }
-        }
-        if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], (nrk - 1) * R * kGroupWarps * 32 * 16);
-        mbar_wait(&xfull[xb], (j >> 1) & 1);  // data and completion are both CTA-local
-        // every rank adds the partials in rank order 0, 1, ...: identical bits on all of them
-        // (two ranks: own + other, as IEEE addition commutes)
+          if (w == 0 && lane == 0) mbar_arrive_expect_tx(&xfull[xb], R * kGroupWarps * 32 * 16);
+          mbar_wait(&xfull[xb], (j >> 1) & 1);  // data and completion are both CTA-local
 #pragma unroll
-        for (int ch = 0; ch < R; ++ch) {
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q >= nrk) continue;
-            double2 v;
-            if (q == (int)rank) {
-              v = make_double2(D0[ch], D1[ch]);
-            } else {
-              const int src = q < (int)rank ? q : q - 1;
-              v = lds128(xb_local + (uint32_t)((((((xb * (nrk - 1) + src) * R + ch) * kGroupWarps + w) * 32 + lane) * 16)));
-            }
-            if (q == 0) {
-              a0 = v.x;
-              a1 = v.y;
-            } else {
-              a0 += v.x;
-              a1 += v.y;
-            }
+          for (int ch = 0; ch < R; ++ch) {
+            const uint32_t mine =
+                xb_local + (uint32_t)((((xb * R + ch) * kGroupWarps + w) * 32 + lane) * 16);
+            const double2 o = lds128(mine);
+            D0[ch] += o.x;  // IEEE addition commutes: both ranks hold (rank 0) + (rank 1)
+            D1[ch] += o.y;
           }
-          D0[ch] = a0;
-          D1[ch] = a1;
         }
       }
       if (prof) { const unsigned long long t = clock64(); ph[2] += t - t1; t1 = t; if (tl && j < kTl) tl[j * 6 + 3] = t; }
@@ -753,9 +779,9 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
 #endif
 }
 
-template <int KW, int R, bool CT, int MTW = mtw_for(KW, R)>
+template <int KW, int R, bool CT, int MTW = mtw_for(KW, R), bool QUAD = false>
 static cudaError_t launch_k12(const SplitParams& p, int grid, cudaStream_t st) {
-  auto k = k12_kernel<KW, MTW, R, CT>;
+  auto k = k12_kernel<KW, MTW, R, CT, QUAD>;
   const size_t smem = k12_smem_bytes(p.stages, p.slot_units, R, p.cluster);
   cudaError_t e = ensure_smem(k, smem);
   if (e != cudaSuccess) return e;
@@ -815,8 +841,29 @@ static cudaError_t launch_r(const SplitParams& p, int grid, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+// clusters of 4: R = 1, KW 8..16 with their MTW (and the narrow variants)
+template <bool CT>
+static cudaError_t launch_quad(const SplitParams& p, int grid, cudaStream_t st) {
+  if (p.R != 1) return cudaErrorInvalidValue;
+  const bool narrow = p.mtw == mtw_for(p.kw, 1) - 1;
+  switch (p.kw) {
+#define BGS_KWQ(K)                                                                          \
+  case K:                                                                                   \
+    if constexpr (has_narrow(K, 1))                                                         \
+      if (narrow) return launch_k12<K, 1, CT, mtw_for(K, 1) - 1, true>(p, grid, st);        \
+    if (p.mtw == mtw_for(K, 1)) return launch_k12<K, 1, CT, mtw_for(K, 1), true>(p, grid, st); \
+    break;
+    BGS_KWQ(8) BGS_KWQ(9) BGS_KWQ(10) BGS_KWQ(11) BGS_KWQ(12) BGS_KWQ(13) BGS_KWQ(14) BGS_KWQ(15)
+    BGS_KWQ(16)
+#undef BGS_KWQ
+    default: break;
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <bool CT>
 static cudaError_t launch_any(const SplitParams& p, int grid, cudaStream_t st) {
+  if (p.cluster == 4) return launch_quad<CT>(p, grid, st);
   switch (p.R) {
     case 1: return launch_r<1, CT>(p, grid, st);
     case 2: return launch_r<2, CT>(p, grid, st);
