@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) k12_kernel(const __grid_constant_
     // base and the row offset): lane (i, kk) reads z[row][kk] of both source blocks and owns
     // output columns 2kk, 2kk + 1 (A for kk < 2, B for kk >= 2).  Recomputing these per stage
     // cost ~250 cycles of a ~5000-cycle group-stage (33.8 -> 32.9 ms of fused time at config 2).
-    constexpr bool kEpPlan = MTW <= 6;  // (MTW >= 7: no registers to spare, measured)
+    constexpr bool kEpPlan = MTW <= 6 || (MTW == 7 && KW <= 12);  // (wider: no registers to spare, measured)
     const bool ep_isA = kk < 2;
     const bool ep_za = p.upd_a && kk < s, ep_zb = p.upd_b && kk < s;
     const uint32_t ep_offA = elem_off<2>(colA + kk, erow), ep_offB = elem_off<2>(colB + kk, erow);
