@@ -653,6 +653,18 @@ class Runner {
     c->roots_all.ensure((size_t)P * ss * sizeof(double) + 64);
     c->cross_ws.ensure(tsqr_ws_bytes(P, (int)s) + 64);
     c->cross_m.ensure((size_t)P * ss * sizeof(double) + 64);
+    // BGS_POISON=2 (tests): NaN-fill every workspace at the start of EVERY factorization, not
+    // only when it is allocated: whatever an earlier call left behind (finite, so invisible to
+    // BGS_POISON=1) must not be read before this call writes it.
+    static const int poison_level = [] {
+      const char* e = getenv("BGS_POISON");
+      return e ? atoi(e) : 0;
+    }();
+    if (poison_level >= 2)
+      for (DBuf* b : {&c->G, &c->scolA, &c->scolB, &c->save, &c->sdiag, &c->ydiag, &c->r1, &c->r2,
+                      &c->rtop, &c->partial, &c->tsqr_ws, &c->roots, &c->roots_all, &c->cross_ws,
+                      &c->cross_m, &c->coefws})
+        if (b->p && b->bytes) CUDA_OK(cudaMemsetAsync(b->p, 0xFF, b->bytes, c->stream));
   }
 
   int grid_for(const Shard& x) const {

@@ -809,6 +809,10 @@ cudaError_t tsqr_tree_up_shard(double* ws, int L, int leaf_base, int Lt, int s, 
   return cudaGetLastError();
 }
 
+__global__ void set_identity_kernel(double* M, int s) {
+  for (int e = threadIdx.x; e < s * s; e += blockDim.x) M[e] = (e % s == e / s) ? 1.0 : 0.0;
+}
+
 // Top-down: the shard root's M (mtop, or identity when null) to the leaf M's in the
 // workspace's M region.
 cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s,
@@ -820,9 +824,13 @@ cudaError_t tsqr_tree_down_shard(double* ws, int L, int leaf_base, int Lt, int s
   double* nq = ws + (size_t)4 * L * ss + (size_t)leaf_base * 2 * ss;
   if (Lt <= 1) {
     if (mtop) return cudaMemcpyAsync(M, mtop, ss * sizeof(double), cudaMemcpyDeviceToDevice, st);
-    std::vector<double> id(ss, 0.0);
-    for (int i = 0; i < s; ++i) id[i + (size_t)i * s] = 1.0;
-    return cudaMemcpyAsync(M, id.data(), ss * sizeof(double), cudaMemcpyHostToDevice, st);
+    // (a kernel, not an H2D copy of a host temporary: when the factorization is captured
+    // into a CUDA graph the copy node would keep the pointer of a vector that is gone by
+    // the time the graph runs -- wrong Q for every single-leaf shard on this path, i.e.
+    // s not in {1, 2, 4, 8, 16}, found by the round-2 fuzz through bgs_factor_device)
+    set_identity_kernel<<<1, 256, 0, st>>>(M, s);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
   }
   const TreePlan t = tree_plan(Lt, s);
   const int K = (int)t.launches.size();

@@ -864,6 +864,42 @@ def test_wide_shapes_beyond_staging_match_oracle(oracle, gpu_ctx, v, n, m, s):
     assert abs(out.loo - loo) <= 0.5 * loo + 1e-15 and abs(out.resid - res) <= 0.5 * res + 1e-16
 
 
+@pytest.mark.parametrize("v", [1, 3, 4, 5], ids=lambda v: NAMES[v])
+@pytest.mark.parametrize("n,m,s", [(56, 54, 6), (1000, 30, 3), (300, 48, 8), (20000, 64, 4),
+                                   (3000, 20, 5), (700, 36, 12)])
+def test_graph_replay_with_new_data_equals_plain_launches(v, n, m, s, monkeypatch):
+    """bgs_factor_device captures a CUDA graph on the second call with one signature and
+    replays it afterwards.  The data may differ from call to call: matrix A (plain
+    launches), matrix B (captures), A and B again (replays) on fixed buffers must give the
+    bits of BGS_GRAPH=0.  (Round-2 fuzz, FUZZ_NCCL seed 502 case 1123: the generic TSQR
+    path wrote a single leaf's identity with an H2D copy of a host temporary, which a graph
+    replays from a dead pointer -- wrong Q for s not in {1, 2, 4, 8, 16}.)"""
+    import torch
+
+    import paper_2507_21791_b200 as bgs
+    ctx = bgs.Context(0)
+    ld = (n + 31) // 32 * 32
+    X = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    Q = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    mats = [bgs.gen_gaussian_host(11 + i, n, m) for i in range(2)]
+
+    def sweep():
+        res = []
+        for which in (0, 1, 0, 1):
+            X.zero_()
+            Q.zero_()
+            X[:, :n] = torch.from_numpy(np.ascontiguousarray(mats[which].T)).cuda()
+            r, st, tm = bgs.factor_device(ctx, v, n, m, s, 0, n, X.data_ptr(), ld, Q.data_ptr(), ld)
+            res.append((r.copy(), Q[:, :n].cpu().numpy().copy()))
+        return res
+
+    graph = sweep()
+    monkeypatch.setenv("BGS_GRAPH", "0")
+    plain = sweep()
+    for a, b in zip(graph, plain):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
 def test_ip1s_s8_square_gaussian_loo_within_band(oracle, gpu_ctx):
     """Fuzz case of round 2 (FUZZ_PEER seed 404, case 534): BCGSI+1S, n = m = 80, s = 8, a
     square Gaussian matrix with cond 1.9e3.  With the explicit 2s x 2s factor matrix in the
