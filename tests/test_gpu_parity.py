@@ -732,14 +732,18 @@ def test_host_leading_dimensions(gpu_ctx, pinned):
     assert np.all(rr[:, m:] == -5.0)
 
 
-def test_randomized_parity_fuzz():
+@pytest.mark.parametrize("mode", ["default", "device"])
+def test_randomized_parity_fuzz(mode):
     """200 random (variant, n, m, s, procs, kappa, generator, seed) cases inside each
-    variant's working assumption against the oracle (tools/fuzz_parity.py)."""
+    variant's working assumption against the oracle (tools/fuzz_parity.py).  "device":
+    through bgs_factor_device on fixed buffers, every fourth shape repeated twice with other
+    seeds, so CUDA graphs are captured and replayed on new data (FUZZ_DEVICE=1)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "tools/fuzz_parity.py", "200", "2024"], cwd=root,
+    env = dict(os.environ, **({"FUZZ_DEVICE": "1"} if mode == "device" else {}))
+    r = subprocess.run([sys.executable, "tools/fuzz_parity.py", "200", "2024"], cwd=root, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "failures: 0" in r.stdout, r.stdout[-3000:]
